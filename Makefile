@@ -1,0 +1,40 @@
+# Build of the B200-native library (sm_100a only) and the test-only oracles.
+#
+#   make            -> paper_2310_16238_b200/libstratcox_b200.so  (product)
+#                      oracle/liboracle.so, oracle/_ref/libstratcox_ref.so (tests only)
+#   make lib        -> product library only
+#
+# nvcc cross-compiles sm_100a here; the .so files are git-ignored but travel to
+# the GPU box with the gpurun snapshot.
+
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr \
+             -Xptxas -v
+PKG       := paper_2310_16238_b200
+LIB       := $(PKG)/libstratcox_b200.so
+CSRC      := $(PKG)/csrc
+OBJDIR    := build/obj
+
+.PHONY: all lib oracle clean dropin
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJDIR)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/internal.cuh $(CSRC)/rules.cuh
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/kernels.ptxas.txt || (cat $(OBJDIR)/kernels.ptxas.txt; exit 1)
+
+$(OBJDIR)/capi.o: $(CSRC)/capi.cu $(CSRC)/internal.cuh $(CSRC)/rules.cuh include/stratcox_b200.h
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/capi.ptxas.txt || (cat $(OBJDIR)/capi.ptxas.txt; exit 1)
+
+$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
+
+oracle:
+	$(MAKE) -C oracle oracle
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; else echo "reference absent: using prebuilt oracle/_ref if any"; fi
+
+clean:
+	rm -rf build $(LIB)

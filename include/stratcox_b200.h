@@ -1,0 +1,185 @@
+/*
+ * stratcox_b200 — C-ABI of the B200-native (sm_100a) stratified Cox CCD hot path.
+ *
+ * This is the drop-in boundary. Each entry point replaces one function of the
+ * reference C++ API (namespace stratcox, /root/reference/proj/include/stratcox/);
+ * the reference interface it replaces is cited beside it. Arguments are plain
+ * pointers and sizes — no C++ or torch types — so a C++ shim (see
+ * INTEGRATION.md and paper_2310_16238_b200/csrc/dropin/) or a ctypes/cffi
+ * binding can bind it directly.
+ *
+ * Object model
+ *   scx_ctx     one device + one stream + one uploaded SortedDesign + one
+ *               CoefficientState. Not thread-safe; create one per thread
+ *               (the reference calls ccd_fit concurrently from OpenMP threads,
+ *               proj/src/resample.cpp:121,207 — each gets its own context).
+ *   errors      every call returns scx_status; scx_last_error(ctx) holds the
+ *               message, identical to the reference exception text
+ *               (proj/include/stratcox/errors.hpp:9-26 taxonomy:
+ *               validation_error / numeric_error / internal_error).
+ *
+ * Row space: all row indices are SORTED rows (stratum ascending, time
+ * descending, stable — proj/src/data.cpp:75-81), i.e. a SortedDesign.
+ */
+#ifndef STRATCOX_B200_H
+#define STRATCOX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct scx_ctx scx_ctx;
+
+typedef enum {
+    SCX_OK = 0,
+    SCX_ERR_VALIDATION = 1, /* stratcox::validation_error */
+    SCX_ERR_NUMERIC = 2,    /* stratcox::numeric_error   */
+    SCX_ERR_INTERNAL = 3,   /* stratcox::internal_error  */
+    SCX_ERR_CUDA = 4        /* device/runtime failure (no reference equivalent) */
+} scx_status;
+
+/* ---------------------------------------------------------------- context */
+const char* scx_version(void);
+/* Number of visible CUDA devices (0 when none / no driver). */
+int scx_device_count(void);
+scx_status scx_create(int device, scx_ctx** out);
+void scx_destroy(scx_ctx* ctx);
+const char* scx_last_error(const scx_ctx* ctx);
+
+/* ---------------------------------------------------------------- design
+ * Replaces the device-side view of SortedDesign (data.hpp:50-62) as produced
+ * by build_sorted_design (data.cpp:68-147).
+ *   stratum_offsets  int64[n_strata+1]   SortedDesign::stratum_offsets
+ *   event            uint8[n_rows]       SortedDesign::data.event (0/1)
+ *   tie_group_end    int64[n_rows]       SortedDesign::tie_group_end
+ *   col_ptr          int64[p+1]          concatenation of data.columns[j]
+ *   row_idx          int64[nnz]          SparseColumn::rows (sorted rows, strictly increasing)
+ *   values           double[nnz] or NULL SparseColumn::values (NULL = every value 1.0)
+ * Columns whose values are all 1.0 are stored as indicators (row index only).
+ * Uploading resets the coefficient state to beta = 0. */
+scx_status scx_upload_design(scx_ctx* ctx, int64_t n_rows, int32_t n_strata,
+                             const int64_t* stratum_offsets, const uint8_t* event,
+                             const int64_t* tie_group_end, int64_t n_covariates,
+                             const int64_t* col_ptr, const int64_t* row_idx,
+                             const double* values);
+
+/* Same design, row indices already int32 (no host->device narrowing pass). */
+scx_status scx_upload_design_i32(scx_ctx* ctx, int64_t n_rows, int32_t n_strata,
+                                 const int64_t* stratum_offsets, const uint8_t* event,
+                                 const int64_t* tie_group_end, int64_t n_covariates,
+                                 const int64_t* col_ptr, const int32_t* row_idx,
+                                 const double* values);
+
+/* Design statistics: n_rows, n_strata, p, nnz, event-code width in bytes,
+ * number of 4096-row tiles, indicator-column count. Any pointer may be NULL. */
+scx_status scx_design_info(const scx_ctx* ctx, int64_t* n_rows, int32_t* n_strata, int64_t* p,
+                           int64_t* nnz, int32_t* code_bytes, int64_t* n_tiles,
+                           int64_t* n_indicator);
+
+/* ---------------------------------------------------------------- state
+ * CoefficientState (likelihood.hpp:23-29) lives on the device. */
+/* make_state (likelihood.hpp:33, likelihood.cpp:19-29): beta[p] -> eta, D. */
+scx_status scx_make_state(scx_ctx* ctx, const double* beta);
+/* Load an arbitrary host CoefficientState (used at the parity boundary by the
+ * C++ shim for gradient_hessian / log_partial_likelihood calls). */
+scx_status scx_set_state(scx_ctx* ctx, const double* beta, const double* xbeta,
+                         const double* exp_xbeta, uint32_t updates_since_refresh);
+/* Read the state back; any pointer may be NULL. */
+scx_status scx_get_state(scx_ctx* ctx, double* beta, double* xbeta, double* exp_xbeta,
+                         uint32_t* updates_since_refresh);
+/* refresh_xbeta (likelihood.hpp:37, likelihood.cpp:31-58). */
+scx_status scx_refresh_xbeta(scx_ctx* ctx);
+/* update_xbeta (likelihood.hpp:43-44, likelihood.cpp:60-83): "step overflow"
+ * leaves the state untouched; refresh every 256 accepted updates. */
+scx_status scx_update_xbeta(scx_ctx* ctx, int64_t j, double delta);
+
+/* ---------------------------------------------------------------- likelihood */
+/* gradient_hessian (likelihood.hpp:75-77, likelihood.cpp:129-189). */
+scx_status scx_gradient_hessian(scx_ctx* ctx, int64_t j, double* gradient, double* hessian);
+/* log_partial_likelihood (likelihood.hpp:60-65, likelihood.cpp:93-121). */
+scx_status scx_log_partial_likelihood(scx_ctx* ctx, double* loglik);
+/* naive_gradient_hessian / naive_log_partial_likelihood (likelihood.hpp:80-82,
+ * likelihood.cpp:191-244): literal O(sum n_k^2) risk-set loops, on device. */
+scx_status scx_naive_gradient_hessian(scx_ctx* ctx, int64_t j, double* gradient,
+                                      double* hessian);
+scx_status scx_naive_log_partial_likelihood(scx_ctx* ctx, double* loglik);
+
+/* segmented_inclusive_scan (scan.hpp:71-79, scan.cpp:124-190) on the device.
+ * Host in/out buffers; n >= 1, flags[0] must be 1. Uses the context's stream
+ * and scratch but not its design. */
+scx_status scx_segmented_inclusive_scan(scx_ctx* ctx, int64_t n, const double* values,
+                                        const uint8_t* flags, double* out);
+
+/* ---------------------------------------------------------------- optimizer */
+/* Scalar rules (optimizer.hpp:47-68, optimizer.cpp:32-78). The same code runs
+ * on the device inside scx_ccd_fit. */
+scx_status scx_newton_step(double g1, double g2, double* step, int* flat);
+scx_status scx_apply_trust_region(double proposed, double trust, double* applied,
+                                  double* next_trust);
+scx_status scx_l1_coordinate_update(double g1, double g2, double beta_j, double gamma_j,
+                                    double* step, int* skipped, int* flat);
+
+/* Message of the last failing scalar-rule call on this thread. */
+const char* scx_rule_error(void);
+
+typedef struct {
+    int32_t max_cycles;   /* OptimizerConfig::max_cycles   (default 1000) */
+    double tolerance;     /* OptimizerConfig::tolerance    (default 1e-6) */
+    double initial_trust; /* OptimizerConfig::initial_trust (default 1.0) */
+} scx_fit_options;
+
+typedef struct {
+    double* beta;            /* [p]  FitResult::beta */
+    double* trust;           /* [p]  FitResult::trust (may be NULL) */
+    double* objective_trace; /* [max_cycles+1] FitResult::objective_trace */
+    int32_t trace_len;       /* entries written */
+    int32_t cycles_used;     /* FitResult::cycles_used */
+    int32_t converged;       /* FitResult::converged */
+    int32_t n_warnings;      /* coordinates skipped after 10 halvings */
+    int64_t* warning_coords; /* [warning_cap] coordinate of each warning, in order (may be NULL) */
+    int32_t warning_cap;
+    uint32_t updates_since_refresh;
+    int64_t n_evaluations;   /* gradient/Hessian evaluations performed (nnz_j > 0 coordinates) */
+} scx_fit_result;
+
+/* ccd_fit (optimizer.hpp:70-73, optimizer.cpp:82-160). gamma[p] = PenaltySpec::gamma;
+ * initial_beta NULL = zeros. The whole cycle runs on the device; the host
+ * synchronises once per cycle (objective, max step, error word). */
+scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options* options,
+                       const double* initial_beta, scx_fit_result* result);
+
+/* gamma_max (resample.hpp:38-39, resample.cpp:42-55) with a penalty template
+ * gamma_template[p] (NULL = every coefficient penalized). */
+scx_status scx_gamma_max(scx_ctx* ctx, const double* gamma_template, double* out);
+
+/* ---------------------------------------------------------------- measurement
+ * Device time of the kernels launched by the last call, for bench/roofline:
+ * per-kernel-class accumulated milliseconds and launch counts since the last
+ * scx_timing_reset. Enabled by scx_timing_enable(ctx, 1) (adds events). */
+scx_status scx_timing_enable(scx_ctx* ctx, int on);
+scx_status scx_timing_reset(scx_ctx* ctx);
+/* kind: 0 = fused scan+reduce (K1), 1 = update (K3), 2 = log-likelihood (K2) */
+scx_status scx_timing_get(scx_ctx* ctx, int kind, double* total_ms, int64_t* launches);
+
+/* Raw device pointers of the context's stream (cudaStream_t) for callers that
+ * want to time on it; returns NULL without a context. */
+void* scx_stream(scx_ctx* ctx);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * Row-sharded fits: each rank uploads the rows of whole strata it owns
+ * (shards split at stratum boundaries, so no scan carry crosses devices) and
+ * exchanges the 16-byte (gradient, Hessian) partials per coordinate. The
+ * exchange sums partials in rank order, so every rank applies a bit-identical
+ * coordinate step. */
+/* 128-byte NCCL unique id, generated on rank 0 and broadcast by the caller. */
+scx_status scx_comm_unique_id(char out[128]);
+scx_status scx_comm_init(scx_ctx* ctx, int nranks, int rank, const char unique_id[128]);
+scx_status scx_comm_destroy(scx_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STRATCOX_B200_H */

@@ -1,0 +1,110 @@
+"""ctypes binding of the C-ABI in include/stratcox_b200.h.
+
+This is the only module that touches the shared library. It loads the in-tree
+``libstratcox_b200.so`` (built by ``make lib`` / ``__graft_entry__.build()``)
+and fails loudly when it is missing: there is no CPU fallback for the product
+path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstratcox_b200.so")
+
+_i8p = C.POINTER(C.c_uint8)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_u32p = C.POINTER(C.c_uint32)
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_vp = C.c_void_p
+
+SCX_OK, SCX_ERR_VALIDATION, SCX_ERR_NUMERIC, SCX_ERR_INTERNAL, SCX_ERR_CUDA = range(5)
+
+
+class FitOptions(C.Structure):
+    _fields_ = [("max_cycles", C.c_int32), ("tolerance", C.c_double), ("initial_trust", C.c_double)]
+
+
+class FitResultC(C.Structure):
+    _fields_ = [
+        ("beta", _dp),
+        ("trust", _dp),
+        ("objective_trace", _dp),
+        ("trace_len", C.c_int32),
+        ("cycles_used", C.c_int32),
+        ("converged", C.c_int32),
+        ("n_warnings", C.c_int32),
+        ("warning_coords", _i64p),
+        ("warning_cap", C.c_int32),
+        ("updates_since_refresh", C.c_uint32),
+        ("n_evaluations", C.c_int64),
+    ]
+
+
+# name -> (restype, argtypes); every symbol declared in include/stratcox_b200.h
+SIGNATURES = {
+    "scx_version": (C.c_char_p, []),
+    "scx_device_count": (C.c_int, []),
+    "scx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "scx_destroy": (None, [_vp]),
+    "scx_last_error": (C.c_char_p, [_vp]),
+    "scx_upload_design": (C.c_int, [_vp, C.c_int64, C.c_int32, _i64p, _i8p, _i64p, C.c_int64,
+                                    _i64p, _i64p, _dp]),
+    "scx_upload_design_i32": (C.c_int, [_vp, C.c_int64, C.c_int32, _i64p, _i8p, _i64p,
+                                        C.c_int64, _i64p, _i32p, _dp]),
+    "scx_design_info": (C.c_int, [_vp, _i64p, _i32p, _i64p, _i64p, _i32p, _i64p, _i64p]),
+    "scx_make_state": (C.c_int, [_vp, _dp]),
+    "scx_set_state": (C.c_int, [_vp, _dp, _dp, _dp, C.c_uint32]),
+    "scx_get_state": (C.c_int, [_vp, _dp, _dp, _dp, _u32p]),
+    "scx_refresh_xbeta": (C.c_int, [_vp]),
+    "scx_update_xbeta": (C.c_int, [_vp, C.c_int64, C.c_double]),
+    "scx_gradient_hessian": (C.c_int, [_vp, C.c_int64, _dp, _dp]),
+    "scx_log_partial_likelihood": (C.c_int, [_vp, _dp]),
+    "scx_naive_gradient_hessian": (C.c_int, [_vp, C.c_int64, _dp, _dp]),
+    "scx_naive_log_partial_likelihood": (C.c_int, [_vp, _dp]),
+    "scx_segmented_inclusive_scan": (C.c_int, [_vp, C.c_int64, _dp, _i8p, _dp]),
+    "scx_newton_step": (C.c_int, [C.c_double, C.c_double, _dp, _ip]),
+    "scx_apply_trust_region": (C.c_int, [C.c_double, C.c_double, _dp, _dp]),
+    "scx_l1_coordinate_update": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, _dp,
+                                           _ip, _ip]),
+    "scx_rule_error": (C.c_char_p, []),
+    "scx_ccd_fit": (C.c_int, [_vp, _dp, C.POINTER(FitOptions), _dp, C.POINTER(FitResultC)]),
+    "scx_gamma_max": (C.c_int, [_vp, _dp, _dp]),
+    "scx_timing_enable": (C.c_int, [_vp, C.c_int]),
+    "scx_timing_reset": (C.c_int, [_vp]),
+    "scx_timing_get": (C.c_int, [_vp, C.c_int, _dp, _i64p]),
+    "scx_stream": (_vp, [_vp]),
+    "scx_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "scx_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
+    "scx_comm_destroy": (C.c_int, [_vp]),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the CUDA library (idempotent). Raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: build the sm_100a library first (make lib or "
+            "__graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def ptr(a, ctype):
+    """Pointer to a contiguous numpy array (or None)."""
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(ctype))

@@ -1,0 +1,1200 @@
+// C-ABI (include/stratcox_b200.h) over the sm_100a kernels in kernels.cu.
+//
+// Host responsibilities only: argument validation with the reference's exact
+// messages, device allocation and upload of the SortedDesign, kernel
+// sequencing on the context's stream, and mapping the device error word back
+// to the reference exception taxonomy (proj/include/stratcox/errors.hpp).
+// No arithmetic of the hot path runs here.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cinttypes>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cudaTypedefs.h>
+
+#include "../../include/stratcox_b200.h"
+#include "internal.cuh"
+
+using namespace scx;
+
+namespace {
+
+constexpr long long kNoRow = 0x7fffffffffffffffLL;
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+typedef int ncclResult_t_;
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t_ (*GetUniqueId)(void*) = nullptr;
+    ncclResult_t_ (*CommInitRank)(void**, int, char[128], int) = nullptr;
+    ncclResult_t_ (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    ncclResult_t_ (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    ncclResult_t_ (*CommDestroy)(void*) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t_) = nullptr;
+    bool load() {
+        if (h) return true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names) {
+            h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) return false;
+        GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+        AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+        AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+        CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+        GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+        return GetUniqueId && CommInitRank && AllGather && AllReduce && CommDestroy;
+    }
+};
+NcclApi g_nccl;
+constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclMax = 2;
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// [npad/16][16] f64 view, box 16 x 256 (one 4096-row tile), 128-B swizzle.
+bool make_tmap(CUtensorMap* m, double* base, int64_t npad) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {16, (cuuint64_t)(npad / 16)};
+    cuuint64_t strides[1] = {16 * sizeof(double)};
+    cuuint32_t box[2] = {16, 256};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class T>
+cudaError_t dmalloc(T** p, size_t count) {
+    return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+}
+
+struct Timer {
+    bool on = false;
+    double ms[3] = {0, 0, 0};
+    int64_t launches[3] = {0, 0, 0};
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> kinds;
+    size_t used = 0;
+};
+
+}  // namespace
+
+struct scx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    bool has_design = false;
+    DesignDev d{};
+    DevCtl* ctl_h = nullptr;  // pinned mirror of d.ctl
+    // host metadata
+    std::vector<ColArgs> cols;
+    std::vector<int32_t> zero_cols;
+    int32_t* zero_cols_d = nullptr;
+    std::vector<int64_t> tie_end_h;  // for error-message row mapping only
+    std::vector<uint8_t> event_h;
+    int64_t nnz = 0;
+    int64_t n_indicator = 0;
+    double* xdense = nullptr;
+    double* out2 = nullptr;
+    int64_t* col_beg_d = nullptr;
+    int64_t* val_off_d = nullptr;
+    int64_t* offsets_d = nullptr;
+    int32_t* rows_d = nullptr;
+    double* vals_d = nullptr;
+    int32_t* tptr_d = nullptr;
+    // multi-GPU
+    void* comm = nullptr;
+    int nranks = 1, rank = 0;
+    double* parts_d = nullptr;  // [nranks][4]
+    Timer timer;
+};
+
+namespace {
+
+scx_status fail(scx_ctx* c, scx_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+scx_status cuda_fail(scx_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, SCX_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                                   \
+    do {                                                           \
+        cudaError_t _e = (expr);                                   \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);   \
+    } while (0)
+
+void free_design(scx_ctx* ctx) {
+    DesignDev& d = ctx->d;
+    void* ptrs[] = {d.code,   d.D,          d.eta,         d.beta,      d.gamma,
+                    d.trust,  d.status,     d.slots,       d.partial,   ctx->xdense,
+                    ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
+                    ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    const DevCtl* keep_ctl = d.ctl;
+    d = DesignDev{};
+    d.ctl = const_cast<DevCtl*>(keep_ctl);
+    ctx->xdense = nullptr;
+    ctx->col_beg_d = nullptr;
+    ctx->val_off_d = nullptr;
+    ctx->offsets_d = nullptr;
+    ctx->rows_d = nullptr;
+    ctx->vals_d = nullptr;
+    ctx->tptr_d = nullptr;
+    ctx->zero_cols_d = nullptr;
+    ctx->parts_d = nullptr;
+    ctx->cols.clear();
+    ctx->zero_cols.clear();
+    ctx->has_design = false;
+}
+
+scx_status sync(scx_ctx* ctx) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SCX_OK;
+}
+
+scx_status read_ctl(scx_ctx* ctx) {
+    CK(cudaMemcpyAsync(ctx->ctl_h, ctx->d.ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SCX_OK;
+}
+
+scx_status clear_error(scx_ctx* ctx) {
+    const int zero = 0;
+    const long long none = kNoRow;
+    CK(cudaMemcpyAsync(&ctx->d.ctl->err_kind, &zero, sizeof(int), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaMemcpyAsync(&ctx->d.ctl->bad_min, &none, sizeof(long long), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SCX_OK;
+}
+
+// First event row i (sorted order) whose tie group ends at s.
+int64_t first_event_row_of_group(const scx_ctx* ctx, int64_t s) {
+    int64_t best = s;
+    for (int64_t r = s; r >= 0 && ctx->tie_end_h[r] == s; --r)
+        if (ctx->event_h[r]) best = r;
+    return best;
+}
+
+// Map a pending device error to the reference's exception text.
+scx_status map_error(scx_ctx* ctx, int j_hint) {
+    const DevCtl& c = *ctx->ctl_h;
+    const int kind = c.err_kind;
+    const long long idx = c.err_idx;
+    char buf[256];
+    scx_status st = SCX_ERR_INTERNAL;
+    switch (kind) {
+        case kErrNonFiniteD:
+            snprintf(buf, sizeof buf, "non-finite input at index %lld", idx);
+            st = SCX_ERR_VALIDATION;
+            break;
+        case kErrBadDenom:
+            snprintf(buf, sizeof buf, "risk-set sum not positive at sorted row %" PRId64,
+                     first_event_row_of_group(ctx, idx));
+            st = SCX_ERR_INTERNAL;
+            break;
+        case kErrNonFiniteGH: {
+            // Diagnose like likelihood.cpp:178-187: a non-positive / non-finite
+            // risk-set sum at an event row is an internal error, else numeric.
+            const int j = (int)idx;
+            clear_error(ctx);
+            const ColArgs& col = ctx->cols[j];
+            launch_k1(ctx->d, col, kK1Diag, ctx->stream);
+            read_ctl(ctx);
+            if (ctx->ctl_h->bad_min != kNoRow) {
+                snprintf(buf, sizeof buf, "risk-set sum not positive at sorted row %" PRId64,
+                         first_event_row_of_group(ctx, ctx->ctl_h->bad_min));
+                st = SCX_ERR_INTERNAL;
+            } else {
+                snprintf(buf, sizeof buf, "non-finite gradient/Hessian for covariate x%d", j + 1);
+                st = SCX_ERR_NUMERIC;
+            }
+            break;
+        }
+        case kErrNonFiniteLL:
+            snprintf(buf, sizeof buf, "non-finite log partial likelihood");
+            st = SCX_ERR_NUMERIC;
+            break;
+        case kErrRuleNewton:
+            snprintf(buf, sizeof buf, "non-finite gradient or Hessian in Newton step");
+            st = SCX_ERR_NUMERIC;
+            break;
+        case kErrRuleTrust:
+            snprintf(buf, sizeof buf, "non-finite trust-region inputs");
+            st = SCX_ERR_NUMERIC;
+            break;
+        case kErrRuleBothNegative:
+            snprintf(buf, sizeof buf, "both directional derivatives negative at the origin");
+            st = SCX_ERR_INTERNAL;
+            break;
+        case kErrLPOverflow:
+            snprintf(buf, sizeof buf, "linear predictor overflow at row %lld", idx);
+            st = SCX_ERR_NUMERIC;
+            break;
+        case kErrStepOverflow:
+            snprintf(buf, sizeof buf, "step overflow");
+            st = SCX_ERR_NUMERIC;
+            break;
+        case kErrNonFiniteStep:
+            snprintf(buf, sizeof buf, "non-finite coordinate step");
+            st = SCX_ERR_NUMERIC;
+            break;
+        case kErrBadTieEnd:
+            snprintf(buf, sizeof buf, "tie_group_end out of range at row %lld", idx);
+            st = SCX_ERR_VALIDATION;
+            break;
+        case kErrBadEvent:
+            snprintf(buf, sizeof buf, "event indicator must be 0 or 1 at row %lld", idx);
+            st = SCX_ERR_VALIDATION;
+            break;
+        case kErrBadRows:
+            snprintf(buf, sizeof buf, "column row indices must be strictly increasing");
+            st = SCX_ERR_VALIDATION;
+            break;
+        default:
+            snprintf(buf, sizeof buf, "device error kind %d (index %lld)", kind, idx);
+    }
+    (void)j_hint;
+    clear_error(ctx);
+    return fail(ctx, st, buf);
+}
+
+scx_status check_device_error(scx_ctx* ctx, int j_hint = -1) {
+    scx_status s = read_ctl(ctx);
+    if (s) return s;
+    if (ctx->ctl_h->err_kind != kErrNone) return map_error(ctx, j_hint);
+    return SCX_OK;
+}
+
+scx_status need_design(scx_ctx* ctx) {
+    if (!ctx) return SCX_ERR_VALIDATION;
+    if (!ctx->has_design) return fail(ctx, SCX_ERR_VALIDATION, "no design uploaded");
+    return SCX_OK;
+}
+
+// timing helpers (bench only)
+void tmark(scx_ctx* ctx, int kind) {
+    Timer& t = ctx->timer;
+    if (!t.on) return;
+    if (t.used + 2 > t.ev.size()) {
+        const size_t add = 4096;
+        for (size_t i = 0; i < add; ++i) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            t.ev.push_back(e);
+        }
+        t.kinds.resize(t.ev.size() / 2);
+    }
+    cudaEventRecord(t.ev[t.used], ctx->stream);
+    t.kinds[t.used / 2] = kind;
+    t.used += 1;
+}
+void tend(scx_ctx* ctx) {
+    Timer& t = ctx->timer;
+    if (!t.on) return;
+    cudaEventRecord(t.ev[t.used], ctx->stream);
+    t.used += 1;
+}
+void tcollect(scx_ctx* ctx) {
+    Timer& t = ctx->timer;
+    if (!t.on || t.used == 0) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (size_t i = 0; i + 1 < t.used; i += 2) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t.ev[i], t.ev[i + 1]);
+        const int k = t.kinds[i / 2];
+        t.ms[k] += ms;
+        t.launches[k] += 1;
+    }
+    t.used = 0;
+}
+
+struct ColStats {
+    double lin;
+    double xmax;
+};
+
+__global__ void k_col_stats(const int32_t* rows, const double* vals, const int64_t* col_beg,
+                            const int64_t* val_off, const uint8_t* event, int64_t p,
+                            ColStats* out) {
+    // one warp per column; lane 0 accumulates x*delta in entry order
+    // (likelihood.cpp:147), lanes gather the next 32 entries.
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = wid; j < p; j += nw) {
+        const int64_t beg = col_beg[j], end = col_beg[j + 1];
+        const int64_t vo = val_off[j];
+        double lin = 0.0, xm = 0.0;
+        for (int64_t b = beg; b < end; b += 32) {
+            const int64_t t = b + lane;
+            double term = 0.0, x = 0.0;
+            if (t < end) {
+                x = vo < 0 ? 1.0 : vals[vo + (t - beg)];
+                term = x * (double)event[rows[t]];
+            }
+            xm = fmax(xm, fabs(x));
+            const int cnt = (int)((end - b) < 32 ? (end - b) : 32);
+            for (int q = 0; q < cnt; ++q) {
+                const double v = __shfl_sync(0xffffffffu, term, q);
+                if (lane == 0) lin += v;
+            }
+        }
+        for (int off = 16; off > 0; off >>= 1) xm = fmax(xm, __shfl_xor_sync(0xffffffffu, xm, off));
+        if (lane == 0) out[j] = ColStats{lin, xm};
+    }
+}
+
+__global__ void k_check_rows(const int32_t* rows, const int64_t* col_beg, int64_t p, int64_t nnz,
+                             int64_t n, DevCtl* ctl) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nnz;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = rows[t];
+        if (r < 0 || r >= n) {
+            set_error(ctl, kErrBadRows, t);
+            continue;
+        }
+        if (t == 0) continue;
+        // is t the first entry of its column?
+        int64_t lo = 0, hi = p;  // largest j with col_beg[j] <= t
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (col_beg[mid] <= t)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        if (col_beg[lo] != t && rows[t - 1] >= r) set_error(ctl, kErrBadRows, t);
+    }
+}
+
+__global__ void k_narrow_checked(int32_t* dst, const int64_t* src, int64_t count, int64_t n,
+                                 DevCtl* ctl) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = src[t];
+        if (r < 0 || r >= n) set_error(ctl, kErrBadRows, t);
+        dst[t] = (int32_t)r;
+    }
+}
+
+__global__ void k_fill(double* p, double v, int64_t n) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x)
+        p[t] = v;
+}
+
+__global__ void k_k3_check(const int32_t* rows, const double* vals, const double* eta,
+                           const ColArgs col, DevCtl* ctl) {
+    const double a = ctl->applied;
+    if (a == 0.0 || ctl->err_kind) return;
+    int hl = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < col.nnz;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const double x = col.indicator ? 1.0 : vals[col.val_off + t];
+        const double e = eta[rows[col.beg + t]];
+        double s = a;
+        int h = 0;
+        for (; h <= kMaxHalvings; ++h) {
+            const double next = e + x * s;
+            if (isfinite(next) && fabs(next) <= kLinearPredictorBound) break;
+            s *= 0.5;
+        }
+        hl = max(hl, h);
+    }
+    for (int off = 16; off > 0; off >>= 1) hl = max(hl, __shfl_xor_sync(0xffffffffu, hl, off));
+    if ((threadIdx.x & 31) == 0 && hl > 0) atomicMax(&ctl->hmax, hl);
+}
+
+}  // namespace
+
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* scx_version(void) { return "stratcox_b200 0.1 (sm_100a)"; }
+
+int scx_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+scx_status scx_create(int device, scx_ctx** out) {
+    if (!out) return SCX_ERR_VALIDATION;
+    *out = nullptr;
+    auto* ctx = new scx_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return SCX_ERR_CUDA;
+    }
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (major != 10) {
+        delete ctx;
+        return SCX_ERR_CUDA;  // sm_100a binary only
+    }
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc((void**)&ctx->d.ctl, sizeof(DevCtl)) != cudaSuccess ||
+        cudaMallocHost((void**)&ctx->ctl_h, sizeof(DevCtl)) != cudaSuccess ||
+        cudaMalloc((void**)&ctx->out2, 4 * sizeof(double)) != cudaSuccess) {
+        delete ctx;
+        return SCX_ERR_CUDA;
+    }
+    DevCtl init;
+    memset(&init, 0, sizeof init);
+    init.epoch = 1;
+    init.bad_min = kNoRow;
+    cudaMemcpy(ctx->d.ctl, &init, sizeof init, cudaMemcpyHostToDevice);
+    *out = ctx;
+    return SCX_OK;
+}
+
+void scx_destroy(scx_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->comm && g_nccl.h) g_nccl.CommDestroy(ctx->comm);
+    free_design(ctx);
+    if (ctx->d.ctl) cudaFree(ctx->d.ctl);
+    if (ctx->out2) cudaFree(ctx->out2);
+    if (ctx->ctl_h) cudaFreeHost(ctx->ctl_h);
+    for (auto e : ctx->timer.ev) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* scx_last_error(const scx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void* scx_stream(scx_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_t* offsets,
+                                const uint8_t* event, const int64_t* tie_end, int64_t p,
+                                const int64_t* col_ptr, const int64_t* row64,
+                                const int32_t* row32, const double* values) {
+    if (!ctx) return SCX_ERR_VALIDATION;
+    cudaSetDevice(ctx->device);
+    if (n < 1) return fail(ctx, SCX_ERR_VALIDATION, "dataset has no rows");
+    if (k < 1) return fail(ctx, SCX_ERR_VALIDATION, "dataset has no strata");
+    if (n > (int64_t)0x7fffffff - kTileRows)
+        return fail(ctx, SCX_ERR_VALIDATION, "row count exceeds the int32 row-index range");
+    if (p < 0) return fail(ctx, SCX_ERR_VALIDATION, "negative covariate count");
+    if (offsets[0] != 0 || offsets[k] != n)
+        return fail(ctx, SCX_ERR_VALIDATION, "stratum offsets must span [0, n_rows]");
+    for (int32_t s = 0; s < k; ++s)
+        if (offsets[s + 1] <= offsets[s])
+            return fail(ctx, SCX_ERR_VALIDATION, "stratum offsets must be strictly increasing");
+    if (col_ptr[0] != 0) return fail(ctx, SCX_ERR_VALIDATION, "col_ptr[0] must be 0");
+    for (int64_t j = 0; j < p; ++j)
+        if (col_ptr[j + 1] < col_ptr[j])
+            return fail(ctx, SCX_ERR_VALIDATION, "col_ptr must be non-decreasing");
+    const int64_t nnz = col_ptr[p];
+    if (nnz > (int64_t)0x7fffffff * 64)
+        return fail(ctx, SCX_ERR_VALIDATION, "too many nonzeros");
+
+    // Column classification (host, input preprocessing): indicator columns
+    // (all values 1.0) keep only row indices; others keep compacted values.
+    std::vector<int64_t> val_off(p, -1);
+    std::vector<double> compact;
+    int64_t n_ind = 0;
+    for (int64_t j = 0; j < p; ++j) {
+        bool ind = true;
+        if (values) {
+            for (int64_t t = col_ptr[j]; t < col_ptr[j + 1]; ++t) {
+                if (!std::isfinite(values[t]))
+                    return fail(ctx, SCX_ERR_VALIDATION,
+                                "column x" + std::to_string(j + 1) + " has a non-finite value");
+                if (values[t] != 1.0) ind = false;
+            }
+        }
+        if (ind) {
+            ++n_ind;
+        } else {
+            val_off[j] = (int64_t)compact.size();
+            compact.insert(compact.end(), values + col_ptr[j], values + col_ptr[j + 1]);
+        }
+    }
+
+    free_design(ctx);
+    DesignDev& d = ctx->d;
+    d.n = n;
+    d.k = k;
+    d.p = p;
+    d.ntiles = (n + kTileRows - 1) / kTileRows;
+    d.npad = d.ntiles * kTileRows;
+    cudaStream_t s = ctx->stream;
+
+    // --- event codes
+    uint8_t* event_d = nullptr;
+    int64_t* tie_d = nullptr;
+    uint32_t* w_d = nullptr;
+    unsigned int* maxw_d = nullptr;
+    CK(dmalloc(&event_d, n));
+    CK(dmalloc(&tie_d, n));
+    CK(dmalloc(&w_d, d.npad));
+    CK(dmalloc(&maxw_d, 1));
+    CK(dmalloc(&ctx->offsets_d, k + 1));
+    CK(cudaMemcpyAsync(event_d, event, n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(tie_d, tie_end, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->offsets_d, offsets, (k + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                       s));
+    CK(cudaMemsetAsync(w_d, 0, d.npad * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(maxw_d, 0, sizeof(unsigned int), s));
+    CK(launch_tie_weights(w_d, event_d, tie_d, n, d.ctl, maxw_d, s));
+    unsigned int maxw = 0;
+    CK(cudaMemcpyAsync(&maxw, maxw_d, sizeof maxw, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    d.code_bytes = maxw <= 0x3fu ? 1 : (maxw <= 0x3fffu ? 2 : 4);
+    CK(cudaMalloc(&d.code, d.npad * d.code_bytes));
+    CK(launch_build_codes(d.code, d.code_bytes, n, d.npad, event_d, tie_d, ctx->offsets_d, k, w_d,
+                          s));
+    ctx->tie_end_h.assign(tie_end, tie_end + n);
+    ctx->event_h.assign(event, event + n);
+
+    // --- CSC
+    CK(dmalloc(&ctx->rows_d, nnz));
+    CK(dmalloc(&ctx->col_beg_d, p + 1));
+    CK(dmalloc(&ctx->val_off_d, p));
+    CK(cudaMemcpyAsync(ctx->col_beg_d, col_ptr, (p + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                       s));
+    CK(cudaMemcpyAsync(ctx->val_off_d, val_off.data(), p * sizeof(int64_t),
+                       cudaMemcpyHostToDevice, s));
+    if (row32) {
+        CK(cudaMemcpyAsync(ctx->rows_d, row32, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    } else if (nnz > 0) {
+        const int64_t chunk = std::min<int64_t>(nnz, (int64_t)1 << 26);
+        int64_t* stage = nullptr;
+        CK(dmalloc(&stage, chunk));
+        for (int64_t off = 0; off < nnz; off += chunk) {
+            const int64_t m = std::min(chunk, nnz - off);
+            CK(cudaMemcpyAsync(stage, row64 + off, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            k_narrow_checked<<<1184, 256, 0, s>>>(ctx->rows_d + off, stage, m, n, d.ctl);
+        }
+        CK(cudaStreamSynchronize(s));
+        cudaFree(stage);
+    }
+    if (nnz > 0) k_check_rows<<<1184, 256, 0, s>>>(ctx->rows_d, ctx->col_beg_d, p, nnz, n, d.ctl);
+    CK(dmalloc(&ctx->vals_d, compact.size()));
+    if (!compact.empty())
+        CK(cudaMemcpyAsync(ctx->vals_d, compact.data(), compact.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, s));
+    ColStats* stats_d = nullptr;
+    CK(dmalloc(&stats_d, p));
+    if (p > 0)
+        k_col_stats<<<1184, 256, 0, s>>>(ctx->rows_d, ctx->vals_d, ctx->col_beg_d, ctx->val_off_d,
+                                          event_d, p, stats_d);
+    std::vector<ColStats> stats(p);
+    if (p > 0)
+        CK(cudaMemcpyAsync(stats.data(), stats_d, p * sizeof(ColStats), cudaMemcpyDeviceToHost, s));
+    CK(dmalloc(&ctx->tptr_d, p * (d.ntiles + 1)));
+    if (p > 0) CK(launch_tile_ptr(ctx->tptr_d, ctx->rows_d, ctx->col_beg_d, p, d.ntiles, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(event_d);
+    cudaFree(tie_d);
+    cudaFree(w_d);
+    cudaFree(maxw_d);
+    cudaFree(stats_d);
+
+    // --- state + scratch
+    CK(dmalloc(&d.D, d.npad));
+    CK(dmalloc(&d.eta, d.npad));
+    CK(dmalloc(&d.beta, p));
+    CK(dmalloc(&d.gamma, p));
+    CK(dmalloc(&d.trust, p));
+    CK(dmalloc(&d.status, d.ntiles));
+    CK(dmalloc(&d.slots, 2 * d.ntiles * 4));
+    CK(dmalloc(&d.partial, 2 * d.ntiles));
+    CK(dmalloc(&ctx->xdense, d.npad));
+    CK(cudaMemsetAsync(d.D, 0, d.npad * sizeof(double), s));
+    CK(cudaMemsetAsync(d.eta, 0, d.npad * sizeof(double), s));
+    CK(cudaMemsetAsync(d.beta, 0, std::max<int64_t>(p, 1) * sizeof(double), s));
+    CK(cudaMemsetAsync(d.gamma, 0, std::max<int64_t>(p, 1) * sizeof(double), s));
+    CK(cudaMemsetAsync(d.status, 0, d.ntiles * sizeof(unsigned int), s));
+    d.rows = ctx->rows_d;
+    d.vals = ctx->vals_d;
+    d.tptr = ctx->tptr_d;
+    d.col_beg = ctx->col_beg_d;
+    d.val_off = ctx->val_off_d;
+    d.offsets = ctx->offsets_d;
+    if (!make_tmap(&d.tmap_D, d.D, d.npad) || !make_tmap(&d.tmap_eta, d.eta, d.npad))
+        return fail(ctx, SCX_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+
+    // co-resident block count for the cooperative kernels
+    {
+        int sms = 0, b1 = 0, b2 = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k3_apply_ptr(), kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, refresh_ptr(), kThreads, 0);
+        const int per = std::max(1, std::min(std::min(b1, b2), 2));
+        d.coop_blocks = sms * per;
+    }
+
+    ctx->cols.resize(p);
+    ctx->zero_cols.clear();
+    for (int64_t j = 0; j < p; ++j) {
+        ColArgs c;
+        c.beg = col_ptr[j];
+        c.nnz = col_ptr[j + 1] - col_ptr[j];
+        c.val_off = val_off[j];
+        c.lin = stats[j].lin;
+        c.xmax = stats[j].xmax;
+        c.j = (int32_t)j;
+        c.indicator = val_off[j] < 0 ? 1 : 0;
+        ctx->cols[j] = c;
+        if (c.nnz == 0) ctx->zero_cols.push_back((int32_t)j);
+    }
+    CK(dmalloc(&ctx->zero_cols_d, ctx->zero_cols.size()));
+    if (!ctx->zero_cols.empty())
+        CK(cudaMemcpyAsync(ctx->zero_cols_d, ctx->zero_cols.data(),
+                           ctx->zero_cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    ctx->nnz = nnz;
+    ctx->n_indicator = n_ind;
+    ctx->has_design = true;
+    scx_status st = check_device_error(ctx);
+    if (st) {
+        free_design(ctx);
+        return st;
+    }
+    // state at beta = 0 (make_state)
+    CK(launch_refresh(d, s));
+    return check_device_error(ctx);
+}
+
+scx_status scx_upload_design(scx_ctx* ctx, int64_t n_rows, int32_t n_strata,
+                             const int64_t* stratum_offsets, const uint8_t* event,
+                             const int64_t* tie_group_end, int64_t n_covariates,
+                             const int64_t* col_ptr, const int64_t* row_idx,
+                             const double* values) {
+    return upload_common(ctx, n_rows, n_strata, stratum_offsets, event, tie_group_end,
+                         n_covariates, col_ptr, row_idx, nullptr, values);
+}
+
+scx_status scx_upload_design_i32(scx_ctx* ctx, int64_t n_rows, int32_t n_strata,
+                                 const int64_t* stratum_offsets, const uint8_t* event,
+                                 const int64_t* tie_group_end, int64_t n_covariates,
+                                 const int64_t* col_ptr, const int32_t* row_idx,
+                                 const double* values) {
+    return upload_common(ctx, n_rows, n_strata, stratum_offsets, event, tie_group_end,
+                         n_covariates, col_ptr, nullptr, row_idx, values);
+}
+
+scx_status scx_design_info(const scx_ctx* ctx, int64_t* n_rows, int32_t* n_strata, int64_t* p,
+                           int64_t* nnz, int32_t* code_bytes, int64_t* n_tiles,
+                           int64_t* n_indicator) {
+    if (!ctx || !ctx->has_design) return SCX_ERR_VALIDATION;
+    if (n_rows) *n_rows = ctx->d.n;
+    if (n_strata) *n_strata = ctx->d.k;
+    if (p) *p = ctx->d.p;
+    if (nnz) *nnz = ctx->nnz;
+    if (code_bytes) *code_bytes = ctx->d.code_bytes;
+    if (n_tiles) *n_tiles = ctx->d.ntiles;
+    if (n_indicator) *n_indicator = ctx->n_indicator;
+    return SCX_OK;
+}
+
+// ---------------------------------------------------------------- state
+scx_status scx_make_state(scx_ctx* ctx, const double* beta) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    DesignDev& d = ctx->d;
+    if (d.p > 0) CK(cudaMemcpyAsync(d.beta, beta, d.p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_refresh(d, ctx->stream));
+    return check_device_error(ctx);
+}
+
+scx_status scx_set_state(scx_ctx* ctx, const double* beta, const double* xbeta,
+                         const double* exp_xbeta, uint32_t updates) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    DesignDev& d = ctx->d;
+    cudaStream_t s = ctx->stream;
+    if (d.p > 0) CK(cudaMemcpyAsync(d.beta, beta, d.p * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d.eta, xbeta, d.n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d.D, exp_xbeta, d.n * sizeof(double), cudaMemcpyHostToDevice, s));
+    double m = 0.0;
+    for (int64_t i = 0; i < d.n; ++i) {
+        const double a = std::fabs(xbeta[i]);
+        if (!(a <= m)) m = a;  // NaN propagates as an unusable bound
+    }
+    if (!std::isfinite(m)) m = INFINITY;
+    CK(cudaMemcpyAsync(&d.ctl->mbound, &m, sizeof m, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(&d.ctl->updates, &updates, sizeof updates, cudaMemcpyHostToDevice, s));
+    return sync(ctx);
+}
+
+scx_status scx_get_state(scx_ctx* ctx, double* beta, double* xbeta, double* exp_xbeta,
+                         uint32_t* updates) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    DesignDev& d = ctx->d;
+    cudaStream_t s = ctx->stream;
+    if (beta && d.p > 0)
+        CK(cudaMemcpyAsync(beta, d.beta, d.p * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (xbeta) CK(cudaMemcpyAsync(xbeta, d.eta, d.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (exp_xbeta)
+        CK(cudaMemcpyAsync(exp_xbeta, d.D, d.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (updates)
+        CK(cudaMemcpyAsync(updates, &d.ctl->updates, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    return sync(ctx);
+}
+
+scx_status scx_refresh_xbeta(scx_ctx* ctx) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    CK(launch_refresh(ctx->d, ctx->stream));
+    return check_device_error(ctx);
+}
+
+scx_status scx_update_xbeta(scx_ctx* ctx, int64_t j, double delta) {
+    if (scx_status s = need_design(ctx)) return s;
+    if (j < 0 || j >= ctx->d.p) return fail(ctx, SCX_ERR_VALIDATION, "covariate index out of range");
+    if (!std::isfinite(delta)) return fail(ctx, SCX_ERR_NUMERIC, "non-finite coordinate step");
+    cudaSetDevice(ctx->device);
+    const int zero = 0;
+    CK(cudaMemcpyAsync(&ctx->d.ctl->hmax, &zero, sizeof zero, cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_k3(ctx->d, ctx->cols[j], 1, delta, ctx->stream));
+    return check_device_error(ctx);
+}
+
+// ---------------------------------------------------------------- likelihood
+scx_status scx_gradient_hessian(scx_ctx* ctx, int64_t j, double* g, double* h) {
+    if (scx_status s = need_design(ctx)) return s;
+    if (j < 0 || j >= ctx->d.p) return fail(ctx, SCX_ERR_VALIDATION, "covariate index out of range");
+    cudaSetDevice(ctx->device);
+    tmark(ctx, 0);
+    CK(launch_k1(ctx->d, ctx->cols[j], kK1Eval, ctx->stream));
+    tend(ctx);
+    tcollect(ctx);
+    if (scx_status s = check_device_error(ctx, (int)j)) return s;
+    *g = ctx->ctl_h->g;
+    *h = ctx->ctl_h->h;
+    return SCX_OK;
+}
+
+scx_status scx_log_partial_likelihood(scx_ctx* ctx, double* ll) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    tmark(ctx, 2);
+    CK(launch_k2(ctx->d, 0, ctx->stream));
+    tend(ctx);
+    tcollect(ctx);
+    if (scx_status s = check_device_error(ctx)) return s;
+    *ll = ctx->ctl_h->ll;
+    return SCX_OK;
+}
+
+scx_status scx_naive_gradient_hessian(scx_ctx* ctx, int64_t j, double* g, double* h) {
+    if (scx_status s = need_design(ctx)) return s;
+    if (j < 0 || j >= ctx->d.p) return fail(ctx, SCX_ERR_VALIDATION, "covariate index out of range");
+    cudaSetDevice(ctx->device);
+    CK(launch_naive_gh(ctx->d, ctx->cols[j], ctx->xdense, ctx->out2, ctx->stream));
+    double o[2];
+    CK(cudaMemcpyAsync(o, ctx->out2, sizeof o, cudaMemcpyDeviceToHost, ctx->stream));
+    if (scx_status s = sync(ctx)) return s;
+    *g = o[0];
+    *h = o[1];
+    return SCX_OK;
+}
+
+scx_status scx_naive_log_partial_likelihood(scx_ctx* ctx, double* ll) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    CK(launch_naive_ll(ctx->d, ctx->out2, ctx->stream));
+    double o[2];
+    CK(cudaMemcpyAsync(o, ctx->out2, sizeof o, cudaMemcpyDeviceToHost, ctx->stream));
+    if (scx_status s = sync(ctx)) return s;
+    *ll = o[0];
+    return SCX_OK;
+}
+
+scx_status scx_segmented_inclusive_scan(scx_ctx* ctx, int64_t n, const double* values,
+                                        const uint8_t* flags, double* out) {
+    if (!ctx) return SCX_ERR_VALIDATION;
+    if (n < 1) return fail(ctx, SCX_ERR_VALIDATION, "empty scan input");
+    if (!flags[0]) return fail(ctx, SCX_ERR_VALIDATION, "first element must head a segment");
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    DesignDev t{};
+    t.n = n;
+    t.ntiles = (n + kTileRows - 1) / kTileRows;
+    t.npad = t.ntiles * kTileRows;
+    t.code_bytes = 1;
+    t.ctl = ctx->d.ctl;
+    std::vector<uint8_t> code(t.npad, 0);
+    for (int64_t i = 0; i < n; ++i) code[i] = flags[i] ? 0x80 : 0;
+    double* outd = nullptr;
+    CK(dmalloc(&t.D, t.npad));
+    CK(cudaMalloc(&t.code, t.npad));
+    CK(dmalloc(&t.status, t.ntiles));
+    CK(dmalloc(&t.slots, 2 * t.ntiles * 4));
+    CK(dmalloc(&t.partial, 2 * t.ntiles));
+    CK(dmalloc(&outd, t.npad));
+    CK(cudaMemsetAsync(t.D, 0, t.npad * sizeof(double), s));
+    CK(cudaMemsetAsync(t.status, 0, t.ntiles * sizeof(unsigned int), s));
+    CK(cudaMemcpyAsync(t.D, values, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(t.code, code.data(), t.npad, cudaMemcpyHostToDevice, s));
+    scx_status st = SCX_OK;
+    if (!make_tmap(&t.tmap_D, t.D, t.npad)) {
+        st = fail(ctx, SCX_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    } else {
+        t.tmap_eta = t.tmap_D;
+        cudaError_t e = launch_scan_primitive(t, outd, s);
+        if (e != cudaSuccess) st = cuda_fail(ctx, e, "scan");
+        if (!st) {
+            cudaMemcpyAsync(out, outd, n * sizeof(double), cudaMemcpyDeviceToHost, s);
+            st = read_ctl(ctx);
+            if (!st && ctx->ctl_h->bad_min != kNoRow) {
+                const long long bm = ctx->ctl_h->bad_min;
+                clear_error(ctx);
+                st = fail(ctx, SCX_ERR_VALIDATION, "non-finite input at index " + std::to_string(bm));
+            }
+        }
+    }
+    cudaFree(t.D);
+    cudaFree(t.code);
+    cudaFree(t.status);
+    cudaFree(t.slots);
+    cudaFree(t.partial);
+    cudaFree(outd);
+    return st;
+}
+
+// ---------------------------------------------------------------- scalar rules
+static scx_status rule_status(int rc, const char** msg) {
+    switch (rc) {
+        case kRuleNonFiniteNewton:
+            *msg = "non-finite gradient or Hessian in Newton step";
+            return SCX_ERR_NUMERIC;
+        case kRuleNonFiniteTrust:
+            *msg = "non-finite trust-region inputs";
+            return SCX_ERR_NUMERIC;
+        case kRuleBothNegative:
+            *msg = "both directional derivatives negative at the origin";
+            return SCX_ERR_INTERNAL;
+        default:
+            *msg = "";
+            return SCX_OK;
+    }
+}
+
+static thread_local std::string g_rule_msg;
+
+scx_status scx_newton_step(double g1, double g2, double* step, int* flat) {
+    int fl = 0;
+    const char* m;
+    const scx_status s = rule_status(newton_step(g1, g2, step, &fl), &m);
+    if (flat) *flat = fl;
+    g_rule_msg = m;
+    return s;
+}
+
+scx_status scx_apply_trust_region(double proposed, double trust, double* applied,
+                                  double* next_trust) {
+    double nt = 0.0;
+    const char* m;
+    const scx_status s = rule_status(apply_trust_region(proposed, trust, applied, &nt), &m);
+    if (next_trust) *next_trust = nt;
+    g_rule_msg = m;
+    return s;
+}
+
+scx_status scx_l1_coordinate_update(double g1, double g2, double beta_j, double gamma_j,
+                                    double* step, int* skipped, int* flat) {
+    int sk = 0, fl = 0;
+    const char* m;
+    const scx_status s =
+        rule_status(l1_coordinate_update(g1, g2, beta_j, gamma_j, step, &sk, &fl), &m);
+    if (skipped) *skipped = sk;
+    if (flat) *flat = fl;
+    g_rule_msg = m;
+    return s;
+}
+
+const char* scx_rule_error(void) { return g_rule_msg.c_str(); }
+
+// ---------------------------------------------------------------- fit
+static scx_status run_cycle_tail(scx_ctx* ctx, bool end_of_cycle, double* ll, double* pen,
+                                 double* max_step) {
+    DesignDev& d = ctx->d;
+    cudaStream_t s = ctx->stream;
+    // zero columns: gradient (0, 0) -> flat -> applied 0 -> trust halves
+    // (optimizer.cpp:103-124); batched at the end of the cycle.
+    if (end_of_cycle)
+        CK(launch_trust_halve(d.trust, ctx->zero_cols_d, (int64_t)ctx->zero_cols.size(), s));
+    if (ctx->nranks > 1) {
+        // log-likelihood and max|eta| are rank-local: gather and reduce in rank order
+        tmark(ctx, 2);
+        CK(launch_k2(d, 1, s));
+        tend(ctx);
+        if (scx_status st = read_ctl(ctx)) return st;
+        // (device-side K2 already wrote ll/penalty/mbound into ctl)
+        double send[4] = {ctx->ctl_h->ll, ctx->ctl_h->mbound, 0.0, 0.0};
+        CK(cudaMemcpyAsync(ctx->parts_d + 4 * ctx->rank, send, sizeof send, cudaMemcpyHostToDevice, s));
+        if (g_nccl.AllGather(ctx->parts_d + 4 * ctx->rank, ctx->parts_d, 4, kNcclFloat64, ctx->comm,
+                             s) != 0)
+            return fail(ctx, SCX_ERR_CUDA, "ncclAllGather failed");
+        std::vector<double> all(4 * ctx->nranks);
+        CK(cudaMemcpyAsync(all.data(), ctx->parts_d, all.size() * sizeof(double),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double L = 0.0, M = 0.0;
+        for (int r = 0; r < ctx->nranks; ++r) {
+            L += all[4 * r];
+            M = std::max(M, all[4 * r + 1]);
+        }
+        CK(cudaMemcpyAsync(&d.ctl->mbound, &M, sizeof M, cudaMemcpyHostToDevice, s));
+        if (ctx->ctl_h->err_kind) return map_error(ctx, -1);
+        *ll = L;
+        *pen = ctx->ctl_h->penalty;
+        *max_step = ctx->ctl_h->max_step;
+        return SCX_OK;
+    }
+    tmark(ctx, 2);
+    CK(launch_k2(d, 1, s));
+    tend(ctx);
+    if (scx_status st = check_device_error(ctx)) return st;
+    *ll = ctx->ctl_h->ll;
+    *pen = ctx->ctl_h->penalty;
+    *max_step = ctx->ctl_h->max_step;
+    return SCX_OK;
+}
+
+static scx_status run_coordinate(scx_ctx* ctx, const ColArgs& col) {
+    DesignDev& d = ctx->d;
+    cudaStream_t s = ctx->stream;
+    if (ctx->nranks == 1) {
+        tmark(ctx, 0);
+        CK(launch_k1(d, col, kK1Fit, s));
+        tend(ctx);
+        tmark(ctx, 1);
+        CK(launch_k3(d, col, 0, 0.0, s));
+        tend(ctx);
+        return SCX_OK;
+    }
+    // sharded: local partials -> 32-B allgather -> rank-ordered rule -> exact
+    // overflow check with a max-allreduce of the halving level -> apply.
+    tmark(ctx, 0);
+    CK(launch_k1(d, col, kK1Partial, s));
+    tend(ctx);
+    if (g_nccl.AllGather(&d.ctl->part[0], ctx->parts_d, 4, kNcclFloat64, ctx->comm, s) != 0)
+        return fail(ctx, SCX_ERR_CUDA, "ncclAllGather failed");
+    CK(launch_rank_step(d, col, ctx->parts_d, ctx->nranks, s));
+    k_k3_check<<<std::max(1, (int)std::min<int64_t>((col.nnz + 255) / 256, 1184)), 256, 0, s>>>(
+        d.rows, d.vals, d.eta, col, d.ctl);
+    if (g_nccl.AllReduce(&d.ctl->hmax, &d.ctl->hmax, 1, kNcclInt32, kNcclMax, ctx->comm, s) != 0)
+        return fail(ctx, SCX_ERR_CUDA, "ncclAllReduce failed");
+    tmark(ctx, 1);
+    CK(launch_k3_sharded(d, col, s));
+    tend(ctx);
+    return SCX_OK;
+}
+
+scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options* opt,
+                       const double* initial_beta, scx_fit_result* res) {
+    if (scx_status s = need_design(ctx)) return s;
+    DesignDev& d = ctx->d;
+    const int64_t p = d.p;
+    // PenaltySpec::validate + run_ccd argument checks (optimizer.cpp:24-30, 85-88)
+    for (int64_t j = 0; j < p; ++j)
+        if (!std::isfinite(gamma[j]) || gamma[j] < 0.0)
+            return fail(ctx, SCX_ERR_VALIDATION, "penalty weights must be finite and non-negative");
+    if (opt->max_cycles < 1) return fail(ctx, SCX_ERR_VALIDATION, "max_cycles must be >= 1");
+    if (!(opt->tolerance > 0.0)) return fail(ctx, SCX_ERR_VALIDATION, "tolerance must be positive");
+    if (!(opt->initial_trust > 0.0))
+        return fail(ctx, SCX_ERR_VALIDATION, "initial_trust must be positive");
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    res->trace_len = 0;
+    res->cycles_used = 0;
+    res->converged = 0;
+    res->n_warnings = 0;
+    res->n_evaluations = 0;
+
+    std::vector<double> beta0(p, 0.0);
+    if (initial_beta) std::copy(initial_beta, initial_beta + p, beta0.begin());
+    if (p > 0) {
+        CK(cudaMemcpyAsync(d.gamma, gamma, p * sizeof(double), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d.beta, beta0.data(), p * sizeof(double), cudaMemcpyHostToDevice, s));
+        k_fill<<<std::max(1, (int)std::min<int64_t>((p + 255) / 256, 1184)), 256, 0, s>>>(
+            d.trust, opt->initial_trust, p);
+    }
+    {
+        DevCtl* c = d.ctl;
+        const double zero = 0.0;
+        const int izero = 0;
+        const long long lzero = 0;
+        CK(cudaMemcpyAsync(&c->max_step, &zero, sizeof zero, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(&c->n_warn, &izero, sizeof izero, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(&c->n_eval, &lzero, sizeof lzero, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(&c->hmax, &izero, sizeof izero, cudaMemcpyHostToDevice, s));
+    }
+    // make_state (likelihood.cpp:19-29)
+    CK(launch_refresh(d, s));
+    if (scx_status st = check_device_error(ctx)) return st;
+
+    double ll, pen, max_step;
+    if (scx_status st = run_cycle_tail(ctx, false, &ll, &pen, &max_step)) return st;
+    double objective = -ll + pen;
+    res->objective_trace[res->trace_len++] = objective;
+
+    const double zero = 0.0;
+    for (int cycle = 1; cycle <= opt->max_cycles; ++cycle) {
+        CK(cudaMemcpyAsync(&d.ctl->max_step, &zero, sizeof zero, cudaMemcpyHostToDevice, s));
+        for (int64_t j = 0; j < p; ++j) {
+            const ColArgs& col = ctx->cols[j];
+            if (col.nnz == 0) continue;
+            if (scx_status st = run_coordinate(ctx, col)) return st;
+        }
+        if (scx_status st = run_cycle_tail(ctx, true, &ll, &pen, &max_step)) return st;
+        tcollect(ctx);
+        const double next = -ll + pen;
+        if (next > objective + kMonotoneSlack) {
+            char buf[256];
+            snprintf(buf, sizeof buf, "monotonicity violated: objective rose from %f to %f",
+                     objective, next);
+            return fail(ctx, SCX_ERR_NUMERIC, buf);
+        }
+        objective = next;
+        res->objective_trace[res->trace_len++] = objective;
+        res->cycles_used = cycle;
+        if (max_step < opt->tolerance) {
+            res->converged = 1;
+            break;
+        }
+    }
+    if (p > 0) {
+        CK(cudaMemcpyAsync(res->beta, d.beta, p * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (res->trust)
+            CK(cudaMemcpyAsync(res->trust, d.trust, p * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    if (scx_status st = read_ctl(ctx)) return st;
+    res->n_warnings = ctx->ctl_h->n_warn;
+    res->updates_since_refresh = ctx->ctl_h->updates;
+    res->n_evaluations = ctx->ctl_h->n_eval;
+    if (res->warning_coords)
+        for (int w = 0; w < std::min(res->n_warnings, std::min(res->warning_cap, 64)); ++w)
+            res->warning_coords[w] = ctx->ctl_h->warn_coord[w];
+    return SCX_OK;
+}
+
+scx_status scx_gamma_max(scx_ctx* ctx, const double* gamma_template, double* out) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    DesignDev& d = ctx->d;
+    std::vector<double> zero(d.p, 0.0);
+    if (scx_status s = scx_make_state(ctx, zero.data())) return s;
+    double best = 0.0;
+    for (int64_t j = 0; j < d.p; ++j) {
+        if (gamma_template && gamma_template[j] <= 0.0) continue;
+        if (ctx->cols[j].nnz == 0) continue;
+        double g, h;
+        if (scx_status s = scx_gradient_hessian(ctx, j, &g, &h)) return s;
+        best = dmax(best, std::fabs(g));
+    }
+    *out = best;
+    return SCX_OK;
+}
+
+// ---------------------------------------------------------------- timing
+scx_status scx_timing_enable(scx_ctx* ctx, int on) {
+    if (!ctx) return SCX_ERR_VALIDATION;
+    ctx->timer.on = on != 0;
+    return SCX_OK;
+}
+scx_status scx_timing_reset(scx_ctx* ctx) {
+    if (!ctx) return SCX_ERR_VALIDATION;
+    for (int k = 0; k < 3; ++k) {
+        ctx->timer.ms[k] = 0;
+        ctx->timer.launches[k] = 0;
+    }
+    ctx->timer.used = 0;
+    return SCX_OK;
+}
+scx_status scx_timing_get(scx_ctx* ctx, int kind, double* total_ms, int64_t* launches) {
+    if (!ctx || kind < 0 || kind > 2) return SCX_ERR_VALIDATION;
+    tcollect(ctx);
+    *total_ms = ctx->timer.ms[kind];
+    *launches = ctx->timer.launches[kind];
+    return SCX_OK;
+}
+
+// ---------------------------------------------------------------- multi-GPU
+scx_status scx_comm_unique_id(char out[128]) {
+    if (!g_nccl.load()) return SCX_ERR_CUDA;
+    return g_nccl.GetUniqueId(out) == 0 ? SCX_OK : SCX_ERR_CUDA;
+}
+
+scx_status scx_comm_init(scx_ctx* ctx, int nranks, int rank, const char unique_id[128]) {
+    if (!ctx) return SCX_ERR_VALIDATION;
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(ctx, SCX_ERR_VALIDATION, "invalid rank / world size");
+    if (!g_nccl.load()) return fail(ctx, SCX_ERR_CUDA, "libnccl.so.2 not loadable");
+    cudaSetDevice(ctx->device);
+    char id[128];
+    memcpy(id, unique_id, 128);
+    void* comm = nullptr;
+    if (g_nccl.CommInitRank(&comm, nranks, id, rank) != 0)
+        return fail(ctx, SCX_ERR_CUDA, "ncclCommInitRank failed");
+    ctx->comm = comm;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    if (ctx->parts_d) cudaFree(ctx->parts_d);
+    CK(dmalloc(&ctx->parts_d, 4 * nranks));
+    // the halving bound must use the global column maxima so that every rank
+    // takes the same decisions
+    if (ctx->has_design && ctx->d.p > 0) {
+        std::vector<double> xm(ctx->d.p);
+        for (int64_t j = 0; j < ctx->d.p; ++j) xm[j] = ctx->cols[j].xmax;
+        double* xm_d = nullptr;
+        CK(dmalloc(&xm_d, ctx->d.p));
+        CK(cudaMemcpyAsync(xm_d, xm.data(), xm.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        if (g_nccl.AllReduce(xm_d, xm_d, ctx->d.p, kNcclFloat64, kNcclMax, comm, ctx->stream) != 0)
+            return fail(ctx, SCX_ERR_CUDA, "ncclAllReduce failed");
+        CK(cudaMemcpyAsync(xm.data(), xm_d, xm.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(xm_d);
+        for (int64_t j = 0; j < ctx->d.p; ++j) ctx->cols[j].xmax = xm[j];
+    }
+    return SCX_OK;
+}
+
+scx_status scx_comm_destroy(scx_ctx* ctx) {
+    if (!ctx) return SCX_ERR_VALIDATION;
+    if (ctx->comm && g_nccl.h) g_nccl.CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+    ctx->nranks = 1;
+    ctx->rank = 0;
+    return SCX_OK;
+}
+
+}  // extern "C"

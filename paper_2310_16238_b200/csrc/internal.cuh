@@ -1,0 +1,255 @@
+// Internal declarations shared by the sm_100a kernels and the C-ABI host code.
+//
+// Device data layout (one scx_ctx, sorted row space, N padded to a multiple
+// of the 4096-row tile so every tile is full):
+//   D       f64[Npad]  exp(X beta)             (CoefficientState::exp_xbeta)
+//   eta     f64[Npad]  X beta                  (CoefficientState::xbeta)
+//   code    u8/u16/u32[Npad] per-row event code: bit(W-1) = stratum head,
+//           bit(W-2) = event, low W-2 bits = w_s, the number of events whose
+//           tie group ends at row s (sum_{i: tie_end(i)=s} delta_i). The
+//           reference gathers S[tie_end(i)] per event row i
+//           (likelihood.cpp:165-175); re-associating that sum onto tie-group
+//           ends turns the gather into a forward stream (exact algebra).
+//   rows    i32[nnz]   CSC row indices, columns concatenated (SparseColumn::rows)
+//   vals    f64[nval]  values of non-indicator columns only, compacted
+//   tptr    i32[p][ntiles+1]  per column, entry offset of each tile's first row
+//   beta, gamma, trust  f64[p]
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rules.cuh"
+
+namespace scx {
+
+constexpr int kTileRows = 4096;
+constexpr int kThreads = 256;
+constexpr int kRowsPerThread = kTileRows / kThreads;  // 16
+constexpr int kWarps = kThreads / 32;
+constexpr int kLookbackWindows = 4;  // smem stack depth of the look-back
+
+// look-back slot states (low 2 bits of the status word; high 30 bits = epoch)
+constexpr uint32_t kStAgg = 1;
+constexpr uint32_t kStInc = 2;
+
+// Per-column metadata, passed by value to the per-coordinate kernels.
+struct ColArgs {
+    int64_t beg;      // first entry in rows[]
+    int64_t nnz;      // entries
+    int64_t val_off;  // first value in vals[] (-1 for an indicator column)
+    double lin;       // sum_t x_t * delta_{row_t}, in entry order (likelihood.cpp:147)
+    double xmax;      // max_t |x_t|
+    int32_t j;
+    int32_t indicator;
+};
+
+// Device error word: first failure wins.
+enum ErrKind : int {
+    kErrNone = 0,
+    kErrNonFiniteD = 1,        // validation "non-finite input at index i"  (idx = row)
+    kErrBadDenom = 2,          // internal "risk-set sum not positive at sorted row i" (idx = tie end)
+    kErrNonFiniteGH = 3,       // numeric "non-finite gradient/Hessian for covariate NAME" (idx = j)
+    kErrNonFiniteLL = 4,       // numeric "non-finite log partial likelihood"
+    kErrRuleNewton = 5,        // numeric "non-finite gradient or Hessian in Newton step"
+    kErrRuleTrust = 6,         // numeric "non-finite trust-region inputs"
+    kErrRuleBothNegative = 7,  // internal "both directional derivatives negative at the origin"
+    kErrLPOverflow = 8,        // numeric "linear predictor overflow at row s" (idx = row)
+    kErrStepOverflow = 9,      // numeric "step overflow"
+    kErrNonFiniteStep = 10,    // numeric "non-finite coordinate step"
+    kErrBadTieEnd = 20,        // validation: tie_group_end out of range (upload)
+    kErrBadEvent = 21,         // validation: event indicator must be 0 or 1 (upload)
+    kErrBadRows = 22,          // validation: column rows not strictly increasing / out of range
+};
+
+// Control block in device memory (one per context).
+struct DevCtl {
+    // K1/K2 tile tickets, completion counters, look-back epoch
+    unsigned int ticket;
+    unsigned int done;
+    unsigned int epoch;
+    unsigned int pad0;
+    // software grid barrier for cooperative kernels
+    unsigned int bar_count;
+    unsigned int bar_gen;
+    // error word
+    int err_kind;
+    int pad1;
+    long long err_idx;
+    long long bad_min;  // min offending row found by a diagnostic pass
+    // last evaluation
+    double g, h;
+    double ll;
+    double penalty;
+    // coordinate scratch written by K1's last block, read by K3
+    double applied;   // proposed step after the trust clip
+    int fast;         // 1 = bound check proves no row can overflow
+    int hmax;         // slow path: max over entries of the halvings needed
+    int will_refresh; // the update counter hits 256 if this step is applied
+    int pad2;
+    // fit bookkeeping
+    double max_step;        // sup-norm of applied steps this cycle
+    double mbound;          // upper bound on max_s |eta_s|
+    unsigned int updates;   // CoefficientState::updates_since_refresh
+    int n_warn;             // coordinates skipped after 10 halvings
+    long long n_eval;       // gradient/Hessian evaluations
+    double part[4];         // multi-GPU: (local lin, ratio sum, variance sum, 0)
+    long long warn_coord[64];
+};
+
+struct Pref1 {
+    double v0;
+    uint32_t f;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// TMA: 2-D tiled tensor copy global -> shared, completion on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+// 1-D bulk copy global -> shared (size multiple of 16, both 16-B aligned).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const unsigned int* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned int* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Software grid barrier (kernels using it are launched cooperatively, so all
+// blocks are co-resident).
+__device__ __forceinline__ void grid_sync(DevCtl* ctl) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* gen = &ctl->bar_gen;
+        const unsigned int g = *gen;
+        __threadfence();
+        if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
+            ctl->bar_count = 0;
+            __threadfence();
+            atomicAdd(&ctl->bar_gen, 1u);
+        } else {
+            while (*gen == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void set_error(DevCtl* ctl, int kind, long long idx) {
+    if (atomicCAS(&ctl->err_kind, 0, kind) == 0) {
+        ctl->err_idx = idx;
+        __threadfence();
+    }
+}
+
+// ------------------------------------------------------------------ launch API
+// (defined in kernels.cu; all launches on `stream`)
+struct DesignDev {
+    int64_t n;
+    int64_t npad;
+    int64_t ntiles;
+    int64_t p;
+    int32_t k;
+    int32_t code_bytes;
+    void* code;
+    double* D;
+    double* eta;
+    const int32_t* rows;
+    const double* vals;
+    const int32_t* tptr;
+    const int64_t* col_beg;   // [p+1]
+    const int64_t* val_off;   // [p] (-1 indicator)
+    const int64_t* offsets;   // [k+1]
+    double* beta;
+    double* gamma;
+    double* trust;
+    // look-back scratch
+    unsigned int* status;     // [ntiles]
+    double* slots;            // [2][ntiles][4] agg / inc (s0, s1, s2, flag)
+    double* partial;          // [ntiles][2]
+    DevCtl* ctl;
+    CUtensorMap tmap_D;
+    CUtensorMap tmap_eta;
+    int coop_blocks;          // co-resident blocks for the cooperative kernels
+};
+
+enum K1Mode : int { kK1Eval = 0, kK1Fit = 1, kK1Diag = 2, kK1Partial = 3 };
+
+cudaError_t launch_k1(const DesignDev& d, const ColArgs& col, int mode, cudaStream_t s);
+cudaError_t launch_k2(const DesignDev& d, int fit_mode, cudaStream_t s);
+// K3: apply the step decided by K1 (mode 0 = fit with halving, 1 = standalone
+// update_xbeta with delta given, no halving -> "step overflow")
+cudaError_t launch_k3(const DesignDev& d, const ColArgs& col, int mode, double delta,
+                      cudaStream_t s);
+// refresh eta/D from beta (make_state / refresh_xbeta)
+cudaError_t launch_refresh(const DesignDev& d, cudaStream_t s);
+cudaError_t launch_naive_gh(const DesignDev& d, const ColArgs& col, double* xdense,
+                            double* out2, cudaStream_t s);
+cudaError_t launch_naive_ll(const DesignDev& d, double* out1, cudaStream_t s);
+cudaError_t launch_trust_halve(double* trust, const int32_t* cols, int64_t ncols,
+                               cudaStream_t s);
+cudaError_t launch_rank_step(const DesignDev& d, const ColArgs& col, const double* parts,
+                             int nranks, cudaStream_t s);
+// design preparation
+cudaError_t launch_build_codes(void* code, int code_bytes, int64_t n, int64_t npad,
+                               const uint8_t* event, const int64_t* tie_end,
+                               const int64_t* offsets, int32_t k, uint32_t* wtmp,
+                               cudaStream_t s);
+cudaError_t launch_tie_weights(uint32_t* w, const uint8_t* event, const int64_t* tie_end, int64_t n,
+                               DevCtl* ctl, unsigned int* maxw, cudaStream_t s);
+cudaError_t launch_tile_ptr(int32_t* tptr, const int32_t* rows, const int64_t* col_beg,
+                            int64_t p, int64_t ntiles, cudaStream_t s);
+cudaError_t launch_narrow_rows(int32_t* dst, const int64_t* src, int64_t count, cudaStream_t s);
+cudaError_t launch_scan_primitive(const DesignDev& d, double* out, cudaStream_t s);
+cudaError_t launch_k3_sharded(const DesignDev& d, const ColArgs& col, cudaStream_t s);
+const void* k3_apply_ptr();
+const void* refresh_ptr();
+
+}  // namespace scx
