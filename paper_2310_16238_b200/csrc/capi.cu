@@ -422,7 +422,7 @@ __global__ void k_k3_check(const int32_t* rows, const double* vals, const double
         double s = a;
         int h = 0;
         for (; h <= kMaxHalvings; ++h) {
-            const double next = e + x * s;
+            const double next = __dadd_rn(e, __dmul_rn(x, s));
             if (isfinite(next) && fabs(next) <= kLinearPredictorBound) break;
             s *= 0.5;
         }

@@ -313,7 +313,11 @@ def test_bad_denominator_is_internal_error(ref, oracle):
     dd = upload(a)
     n = a["n"]
     ex = np.ones(n)
-    ex[:5] = 0.0  # first tie groups have a zero risk-set sum
+    # zero D over the first tie group(s) so their risk-set sum is exactly 0
+    first_end = int(a["tie_end"][0])
+    while not a["event"][:first_end + 1].any():
+        first_end = int(a["tie_end"][first_end + 1])
+    ex[:first_end + 1] = 0.0
     from oracle.oracle_py import OracleError
     with pytest.raises(OracleError) as e:
         oracle.gradient_hessian(d, ex, 0)
