@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark: stratified Cox L1 CCD fit at BASELINE config 4 on B200.
+
+Workload (BASELINE.json configs[3], the shape its metric "at N=10M" is quoted
+on): N = 1e7 rows, p = 1e4 sparse binary indicator covariates at 1% density
+(1e9 nonzeros), K = 1e3 strata, L1 penalty gamma = 0.05 * gamma_max, full CCD
+fit from beta = 0 (reference defaults: tolerance 1e-6, trust 1).
+
+One "step" = one complete ccd_fit (every cycle: p fused scan+reduce
+evaluations, on-device coordinate rule, eta/D update, cycle log-likelihood).
+  value   grad+Hessian evaluations per second over the fit, design resident in
+          HBM (CUDA events on the library's stream; L2 flushed by a 256 MiB
+          write before every step)
+  e2e     the same metric through the public C-ABI from pinned host buffers:
+          design upload (H2D) + fit + coefficient download (D2H) per step
+  roofline  the fused scan+reduce kernel (K1) timed alone with L2 flushed
+          before each launch, algorithmic bytes N*(8 + code bytes) + 4*nnz_j
+          per launch vs the measured HBM copy bandwidth
+  cpu_baseline  the reference (oracle/_ref: unmodified stratcox compiled -O3
+          -fopenmp) on a bounded sample of the same workload (N=1e7, K=1e3,
+          1% density, 32 covariates) with run_benchmark semantics, all cores
+
+--impl reference runs the reference CPU arm only (rank 0), same metric.
+Multi-GPU (torchrun, N>1): rows sharded at stratum boundaries, 32-byte
+NCCL partial exchange per coordinate; total work fixed ("strong").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("CCD fit wall time (s) and grad+Hessian evals/sec at N=10M; "
+          "fused-scan HBM GB/s vs peak")
+WORKLOAD = ("C4: stratified Cox L1 CCD fit, N=1e7 rows, p=1e4 sparse indicator covariates "
+            "(1% density), K=1e3 strata, gamma=0.05*gamma_max, beta0=0, tol=1e-6")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU reference arm
+def reference_sample(n, p_sample, k, density, seed, threads):
+    """Bounded sample of the C4 workload on the reference (oracle/_ref)."""
+    from oracle.oracle_py import Ref
+
+    ref = Ref()
+    t0 = time.perf_counter()
+    ds = ref.simulate(n, p_sample, density, 0.8, k, 0.3, seed)
+    h, _ = ref.build_design(ds)
+    del ds
+    gmax = ref.gamma_max(h, workers=threads)
+    return ref, h, 0.05 * gmax, time.perf_counter() - t0
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n, k, dens = args.n, args.k, args.density
+    p_sample, sweep = 32, args.ref_sweep
+    ref, h, gamma, setup = reference_sample(n, p_sample, k, dens, 11, threads)
+    per = ref.time_iterations(h, gamma, args.warmup + args.steps, sweep, threads)
+    timed = per[args.warmup:]
+    sec_per_eval = float(np.mean(timed))
+    value = 1.0 / sec_per_eval
+    sample = (f"reference stratcox (oracle/_ref, -O3 -fopenmp) on N={n}, K={k}, density {dens}, "
+              f"{p_sample} covariates; each step = {sweep} CCD coordinate iterations "
+              f"(benchmark.cpp:27-41 semantics) at gamma=0.05*gamma_max; setup {setup:.1f}s excluded")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec_per_eval * sweep * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_rows": n, "strata": k, "density": dens,
+                   "sample_covariates": p_sample, "l2_flush": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "fit_wall_s_extrapolated": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def flush_l2(buf):
+    buf.add_(1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--p", type=int, default=10_000)
+    ap.add_argument("--k", type=int, default=1000)
+    ap.add_argument("--density", type=float, default=0.01)
+    ap.add_argument("--gamma-frac", type=float, default=0.05)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-sweep", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-k1", action="store_true",
+                    help="only run K1 evaluations (for ncu); prints nothing")
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import paper_2310_16238_b200 as sx
+    from paper_2310_16238_b200 import _capi, synthetic
+    from paper_2310_16238_b200.sharding import plan_row_shards, shard_design
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    lib = _capi.load()
+    hbm_peak, peak_src = peaks()
+
+    # ---- data (generated on this GPU; each rank builds the same global design)
+    syn = synthetic.generate(args.n, args.p, args.k, args.density, seed=11,
+                             device=f"cuda:{local}")
+    log(f"[bench] generated N={syn.n} p={syn.p} K={syn.k} nnz={syn.nnz} in {syn.gen_seconds:.1f}s")
+    design = syn.sorted_design()
+    if world > 1:
+        lo, hi = plan_row_shards(design.stratum_offsets, world)[rank]
+        design = shard_design(design, lo, hi)
+    t0 = time.perf_counter()
+    dd = sx.DeviceDesign(design, device=local)
+    log(f"[bench] upload {time.perf_counter() - t0:.2f}s info={dd.info()}")
+    h = dd.handle
+    if world > 1:
+        from paper_2310_16238_b200.sharding import init_comm
+        init_comm(dd)
+    info = dd.info()
+    p = design.n_covariates
+
+    # ---- gamma = frac * gamma_max (global across shards)
+    if world == 1:
+        gmax = sx.gamma_max(dd)
+    else:
+        st0 = sx.make_state(dd, np.zeros(p))
+        g = np.array([sx.gradient_hessian(dd, st0, j).gradient if design.col_ptr[j + 1] >
+                      design.col_ptr[j] else 0.0 for j in range(p)])
+        gt = torch.tensor(g, device=f"cuda:{local}")
+        dist.all_reduce(gt)
+        gmax = float(gt.abs().max())
+    gamma = args.gamma_frac * gmax
+    pen = sx.PenaltySpec.shared(p, gamma)
+    cfg = sx.OptimizerConfig()
+    log(f"[bench] gamma_max={gmax:.6g} gamma={gamma:.6g}")
+
+    if args.profile_k1:
+        st = sx.make_state(dd, np.zeros(p))
+        for j in range(0, min(p, 64)):
+            sx.gradient_hessian(dd, st, j)
+        return
+
+    dev = torch.device("cuda", local)
+    l2buf = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+    lib_stream = torch.cuda.ExternalStream(lib.scx_stream(h), device=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---- warm-up fits
+    for _ in range(args.warmup):
+        flush_l2(l2buf)
+        r = sx.ccd_fit(dd, pen, cfg)
+    log(f"[bench] warm-up fit: cycles={r.cycles_used} converged={r.converged} "
+        f"nonzero={int(np.count_nonzero(r.beta))} evals={r.n_evaluations}")
+
+    # ---- timed fits (design resident)
+    times, evals, cycles = [], [], []
+    launches0 = lib.scx_launch_count(h)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(l2buf)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(lib_stream)
+            r = sx.ccd_fit(dd, pen, cfg)
+            e1.record(lib_stream)
+            barrier()
+            ms = e0.elapsed_time(e1)
+            if dist is not None:
+                t = torch.tensor([ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t)
+            times.append(ms)
+            evals.append(r.n_evaluations)
+            cycles.append(r.cycles_used)
+    launches = lib.scx_launch_count(h) - launches0
+    ms_step = float(np.mean(times))
+    value = float(np.mean(evals)) / (ms_step / 1e3)
+    beta_fit = r.beta.copy()
+
+    # ---- roofline: K1 alone, L2 flushed before each launch
+    lib.scx_timing_enable(h, 1)
+    st = sx.make_state(dd, beta_fit)
+    nz_cols = [j for j in range(p) if design.col_ptr[j + 1] > design.col_ptr[j]]
+    sample = nz_cols[:: max(1, len(nz_cols) // 48)][:48]
+    lib.scx_timing_reset(h)
+    for j in sample:
+        flush_l2(l2buf)
+        torch.cuda.synchronize(dev)
+        sx.gradient_hessian(dd, st, j)
+    import ctypes as C
+    tot = C.c_double()
+    nl = C.c_int64()
+    lib.scx_timing_get(h, 0, C.byref(tot), C.byref(nl))
+    k1_ms = tot.value / max(1, nl.value)
+    nnz_mean = float(np.mean([design.col_ptr[j + 1] - design.col_ptr[j] for j in sample]))
+    row_bytes = 8 + info["code_bytes"]
+    alg_bytes = design.n_rows * row_bytes + 4 * nnz_mean
+    achieved = alg_bytes / (k1_ms * 1e-3) / 1e9
+    # K1 inside the fit (warm L2: D stays resident between coordinates)
+    lib.scx_timing_reset(h)
+    sx.ccd_fit(dd, pen, sx.OptimizerConfig(max_cycles=1))
+    lib.scx_timing_get(h, 0, C.byref(tot), C.byref(nl))
+    k1_loop_ms = tot.value / max(1, nl.value)
+    t3 = C.c_double(); n3 = C.c_int64()
+    lib.scx_timing_get(h, 1, C.byref(t3), C.byref(n3))
+    k3_loop_ms = t3.value / max(1, n3.value)
+    lib.scx_timing_enable(h, 0)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_k1_summary.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            if pj.get("n_rows") == design.n_rows:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public API from pinned host buffers
+    e2e_times = []
+    h2d = (design.row_idx.nbytes + design.col_ptr.nbytes + design.stratum_offsets.nbytes +
+           design.event.nbytes + design.tie_group_end.nbytes + 8 * p)
+    d2h = 8 * p * 2 + 8 * (cfg.max_cycles + 1)
+    e2e_evals = []
+    del st
+    dd.close()
+    for _ in range(args.e2e_steps):
+        flush_l2(l2buf)
+        barrier()
+        t0 = time.perf_counter()
+        dd2 = sx.DeviceDesign(design, device=local)
+        if world > 1:
+            from paper_2310_16238_b200.sharding import init_comm
+            init_comm(dd2)
+        r2 = sx.ccd_fit(dd2, pen, cfg)
+        barrier()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t)
+        e2e_times.append(el)
+        e2e_evals.append(r2.n_evaluations)
+        dd2.close()
+    e2e_value = float(np.mean(e2e_evals)) / float(np.mean(e2e_times))
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            ref, rh, rgamma, setup = reference_sample(args.n, 32, args.k, args.density, 11,
+                                                      threads)
+            per = ref.time_iterations(rh, rgamma, 3, args.ref_sweep, threads)
+            cv = 1.0 / float(np.median(per))
+            cpu = {"value": cv, "unit": "evals/s", "cores": threads, "kind": "reference",
+                   "sample": (f"oracle/_ref (unmodified stratcox, -O3 -fopenmp) on N={args.n}, "
+                              f"K={args.k}, density {args.density}, 32 covariates: median of 3 "
+                              f"sweeps x {args.ref_sweep} CCD coordinate iterations "
+                              f"(benchmark.cpp:27-41); setup {setup:.1f}s excluded"),
+                   "fit_wall_s_extrapolated": float(np.mean(evals)) / cv}
+            ref.free_design(rh)
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "evals/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (device generator restating simulate.cpp's model; seed 11)",
+            "config": {"workload": WORKLOAD, "n_rows": args.n, "p": args.p, "strata": args.k,
+                       "density": args.density, "nnz": syn.nnz, "gamma": gamma,
+                       "gamma_max": gmax, "fit_cycles": cycles, "evals_per_step": evals,
+                       "code_bytes": info["code_bytes"],
+                       "l2_flush": "256 MiB write before every timed step and before every "
+                                   "roofline K1 launch",
+                       "parallelism": f"rows sharded at stratum boundaries x{world}"
+                       if world > 1 else "single GPU"},
+            "fit_wall_s": ms_step / 1e3,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "kernel": "k1_grad_hess (fused segmented scan + g'/g'' reduce)",
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "avg_launch_ms": k1_ms, "peak_source": peak_src,
+                         "in_fit_avg_launch_ms": k1_loop_ms,
+                         "in_fit_effective_gbs": alg_bytes / (k1_loop_ms * 1e-3) / 1e9,
+                         "k3_in_fit_avg_launch_ms": k3_loop_ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "seconds_per_step": float(np.mean(e2e_times))},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

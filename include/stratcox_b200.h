@@ -164,6 +164,9 @@ scx_status scx_timing_reset(scx_ctx* ctx);
 /* kind: 0 = fused scan+reduce (K1), 1 = update (K3), 2 = log-likelihood (K2) */
 scx_status scx_timing_get(scx_ctx* ctx, int kind, double* total_ms, int64_t* launches);
 
+/* Number of kernels this context has launched so far (bench bookkeeping). */
+int64_t scx_launch_count(const scx_ctx* ctx);
+
 /* Raw device pointers of the context's stream (cudaStream_t) for callers that
  * want to time on it; returns NULL without a context. */
 void* scx_stream(scx_ctx* ctx);

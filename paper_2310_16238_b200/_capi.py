@@ -77,6 +77,7 @@ SIGNATURES = {
     "scx_timing_reset": (C.c_int, [_vp]),
     "scx_timing_get": (C.c_int, [_vp, C.c_int, _dp, _i64p]),
     "scx_stream": (_vp, [_vp]),
+    "scx_launch_count": (C.c_int64, [_vp]),
     "scx_comm_unique_id": (C.c_int, [C.c_char_p]),
     "scx_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
     "scx_comm_destroy": (C.c_int, [_vp]),

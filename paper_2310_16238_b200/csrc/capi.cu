@@ -127,6 +127,7 @@ struct scx_ctx {
     int nranks = 1, rank = 0;
     double* parts_d = nullptr;  // [nranks][4]
     Timer timer;
+    int64_t launches = 0;  // kernels launched by this context
 };
 
 namespace {
@@ -144,6 +145,13 @@ scx_status cuda_fail(scx_ctx* c, cudaError_t e, const char* where) {
     do {                                                           \
         cudaError_t _e = (expr);                                   \
         if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);   \
+    } while (0)
+
+// kernel launch through the launch_* helpers, counted for bench.py's gpu_launches
+#define KL(n, expr)              \
+    do {                         \
+        ctx->launches += (n);    \
+        CK(expr);                \
     } while (0)
 
 void free_design(scx_ctx* ctx) {
@@ -568,13 +576,13 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
                        s));
     CK(cudaMemsetAsync(w_d, 0, d.npad * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(maxw_d, 0, sizeof(unsigned int), s));
-    CK(launch_tie_weights(w_d, event_d, tie_d, n, d.ctl, maxw_d, s));
+    KL(2, launch_tie_weights(w_d, event_d, tie_d, n, d.ctl, maxw_d, s));
     unsigned int maxw = 0;
     CK(cudaMemcpyAsync(&maxw, maxw_d, sizeof maxw, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     d.code_bytes = maxw <= 0x3fu ? 1 : (maxw <= 0x3fffu ? 2 : 4);
     CK(cudaMalloc(&d.code, d.npad * d.code_bytes));
-    CK(launch_build_codes(d.code, d.code_bytes, n, d.npad, event_d, tie_d, ctx->offsets_d, k, w_d,
+    KL(1, launch_build_codes(d.code, d.code_bytes, n, d.npad, event_d, tie_d, ctx->offsets_d, k, w_d,
                           s));
     ctx->tie_end_h.assign(tie_end, tie_end + n);
     ctx->event_h.assign(event, event + n);
@@ -615,7 +623,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     if (p > 0)
         CK(cudaMemcpyAsync(stats.data(), stats_d, p * sizeof(ColStats), cudaMemcpyDeviceToHost, s));
     CK(dmalloc(&ctx->tptr_d, p * (d.ntiles + 1)));
-    if (p > 0) CK(launch_tile_ptr(ctx->tptr_d, ctx->rows_d, ctx->col_beg_d, p, d.ntiles, s));
+    if (p > 0) KL(1, launch_tile_ptr(ctx->tptr_d, ctx->rows_d, ctx->col_beg_d, p, d.ntiles, s));
     CK(cudaStreamSynchronize(s));
     cudaFree(event_d);
     cudaFree(tie_d);
@@ -684,7 +692,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         return st;
     }
     // state at beta = 0 (make_state)
-    CK(launch_refresh(d, s));
+    KL(1, launch_refresh(d, s));
     return check_device_error(ctx);
 }
 
@@ -726,7 +734,7 @@ scx_status scx_make_state(scx_ctx* ctx, const double* beta) {
     cudaSetDevice(ctx->device);
     DesignDev& d = ctx->d;
     if (d.p > 0) CK(cudaMemcpyAsync(d.beta, beta, d.p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    CK(launch_refresh(d, ctx->stream));
+    KL(1, launch_refresh(d, ctx->stream));
     return check_device_error(ctx);
 }
 
@@ -769,7 +777,7 @@ scx_status scx_get_state(scx_ctx* ctx, double* beta, double* xbeta, double* exp_
 scx_status scx_refresh_xbeta(scx_ctx* ctx) {
     if (scx_status s = need_design(ctx)) return s;
     cudaSetDevice(ctx->device);
-    CK(launch_refresh(ctx->d, ctx->stream));
+    KL(1, launch_refresh(ctx->d, ctx->stream));
     return check_device_error(ctx);
 }
 
@@ -780,7 +788,7 @@ scx_status scx_update_xbeta(scx_ctx* ctx, int64_t j, double delta) {
     cudaSetDevice(ctx->device);
     const int zero = 0;
     CK(cudaMemcpyAsync(&ctx->d.ctl->hmax, &zero, sizeof zero, cudaMemcpyHostToDevice, ctx->stream));
-    CK(launch_k3(ctx->d, ctx->cols[j], 1, delta, ctx->stream));
+    KL(1, launch_k3(ctx->d, ctx->cols[j], 1, delta, ctx->stream));
     return check_device_error(ctx);
 }
 
@@ -790,7 +798,7 @@ scx_status scx_gradient_hessian(scx_ctx* ctx, int64_t j, double* g, double* h) {
     if (j < 0 || j >= ctx->d.p) return fail(ctx, SCX_ERR_VALIDATION, "covariate index out of range");
     cudaSetDevice(ctx->device);
     tmark(ctx, 0);
-    CK(launch_k1(ctx->d, ctx->cols[j], kK1Eval, ctx->stream));
+    KL(1, launch_k1(ctx->d, ctx->cols[j], kK1Eval, ctx->stream));
     tend(ctx);
     tcollect(ctx);
     if (scx_status s = check_device_error(ctx, (int)j)) return s;
@@ -803,7 +811,7 @@ scx_status scx_log_partial_likelihood(scx_ctx* ctx, double* ll) {
     if (scx_status s = need_design(ctx)) return s;
     cudaSetDevice(ctx->device);
     tmark(ctx, 2);
-    CK(launch_k2(ctx->d, 0, ctx->stream));
+    KL(1, launch_k2(ctx->d, 0, ctx->stream));
     tend(ctx);
     tcollect(ctx);
     if (scx_status s = check_device_error(ctx)) return s;
@@ -815,7 +823,7 @@ scx_status scx_naive_gradient_hessian(scx_ctx* ctx, int64_t j, double* g, double
     if (scx_status s = need_design(ctx)) return s;
     if (j < 0 || j >= ctx->d.p) return fail(ctx, SCX_ERR_VALIDATION, "covariate index out of range");
     cudaSetDevice(ctx->device);
-    CK(launch_naive_gh(ctx->d, ctx->cols[j], ctx->xdense, ctx->out2, ctx->stream));
+    KL(2, launch_naive_gh(ctx->d, ctx->cols[j], ctx->xdense, ctx->out2, ctx->stream));
     double o[2];
     CK(cudaMemcpyAsync(o, ctx->out2, sizeof o, cudaMemcpyDeviceToHost, ctx->stream));
     if (scx_status s = sync(ctx)) return s;
@@ -827,7 +835,7 @@ scx_status scx_naive_gradient_hessian(scx_ctx* ctx, int64_t j, double* g, double
 scx_status scx_naive_log_partial_likelihood(scx_ctx* ctx, double* ll) {
     if (scx_status s = need_design(ctx)) return s;
     cudaSetDevice(ctx->device);
-    CK(launch_naive_ll(ctx->d, ctx->out2, ctx->stream));
+    KL(1, launch_naive_ll(ctx->d, ctx->out2, ctx->stream));
     double o[2];
     CK(cudaMemcpyAsync(o, ctx->out2, sizeof o, cudaMemcpyDeviceToHost, ctx->stream));
     if (scx_status s = sync(ctx)) return s;
@@ -948,11 +956,11 @@ static scx_status run_cycle_tail(scx_ctx* ctx, bool end_of_cycle, double* ll, do
     // zero columns: gradient (0, 0) -> flat -> applied 0 -> trust halves
     // (optimizer.cpp:103-124); batched at the end of the cycle.
     if (end_of_cycle)
-        CK(launch_trust_halve(d.trust, ctx->zero_cols_d, (int64_t)ctx->zero_cols.size(), s));
+        KL(1, launch_trust_halve(d.trust, ctx->zero_cols_d, (int64_t)ctx->zero_cols.size(), s));
     if (ctx->nranks > 1) {
         // log-likelihood and max|eta| are rank-local: gather and reduce in rank order
         tmark(ctx, 2);
-        CK(launch_k2(d, 1, s));
+        KL(1, launch_k2(d, 1, s));
         tend(ctx);
         if (scx_status st = read_ctl(ctx)) return st;
         // (device-side K2 already wrote ll/penalty/mbound into ctl)
@@ -978,7 +986,7 @@ static scx_status run_cycle_tail(scx_ctx* ctx, bool end_of_cycle, double* ll, do
         return SCX_OK;
     }
     tmark(ctx, 2);
-    CK(launch_k2(d, 1, s));
+    KL(1, launch_k2(d, 1, s));
     tend(ctx);
     if (scx_status st = check_device_error(ctx)) return st;
     *ll = ctx->ctl_h->ll;
@@ -992,27 +1000,28 @@ static scx_status run_coordinate(scx_ctx* ctx, const ColArgs& col) {
     cudaStream_t s = ctx->stream;
     if (ctx->nranks == 1) {
         tmark(ctx, 0);
-        CK(launch_k1(d, col, kK1Fit, s));
+        KL(1, launch_k1(d, col, kK1Fit, s));
         tend(ctx);
         tmark(ctx, 1);
-        CK(launch_k3(d, col, 0, 0.0, s));
+        KL(1, launch_k3(d, col, 0, 0.0, s));
         tend(ctx);
         return SCX_OK;
     }
     // sharded: local partials -> 32-B allgather -> rank-ordered rule -> exact
     // overflow check with a max-allreduce of the halving level -> apply.
     tmark(ctx, 0);
-    CK(launch_k1(d, col, kK1Partial, s));
+    KL(1, launch_k1(d, col, kK1Partial, s));
     tend(ctx);
     if (g_nccl.AllGather(&d.ctl->part[0], ctx->parts_d, 4, kNcclFloat64, ctx->comm, s) != 0)
         return fail(ctx, SCX_ERR_CUDA, "ncclAllGather failed");
-    CK(launch_rank_step(d, col, ctx->parts_d, ctx->nranks, s));
+    KL(1, launch_rank_step(d, col, ctx->parts_d, ctx->nranks, s));
+    ctx->launches += 1;
     k_k3_check<<<std::max(1, (int)std::min<int64_t>((col.nnz + 255) / 256, 1184)), 256, 0, s>>>(
         d.rows, d.vals, d.eta, col, d.ctl);
     if (g_nccl.AllReduce(&d.ctl->hmax, &d.ctl->hmax, 1, kNcclInt32, kNcclMax, ctx->comm, s) != 0)
         return fail(ctx, SCX_ERR_CUDA, "ncclAllReduce failed");
     tmark(ctx, 1);
-    CK(launch_k3_sharded(d, col, s));
+    KL(1, launch_k3_sharded(d, col, s));
     tend(ctx);
     return SCX_OK;
 }
@@ -1045,6 +1054,7 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
         CK(cudaMemcpyAsync(d.beta, beta0.data(), p * sizeof(double), cudaMemcpyHostToDevice, s));
         k_fill<<<std::max(1, (int)std::min<int64_t>((p + 255) / 256, 1184)), 256, 0, s>>>(
             d.trust, opt->initial_trust, p);
+        ctx->launches += 1;
     }
     {
         DevCtl* c = d.ctl;
@@ -1057,7 +1067,7 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
         CK(cudaMemcpyAsync(&c->hmax, &izero, sizeof izero, cudaMemcpyHostToDevice, s));
     }
     // make_state (likelihood.cpp:19-29)
-    CK(launch_refresh(d, s));
+    KL(1, launch_refresh(d, s));
     if (scx_status st = check_device_error(ctx)) return st;
 
     double ll, pen, max_step;
@@ -1124,6 +1134,8 @@ scx_status scx_gamma_max(scx_ctx* ctx, const double* gamma_template, double* out
 }
 
 // ---------------------------------------------------------------- timing
+int64_t scx_launch_count(const scx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
 scx_status scx_timing_enable(scx_ctx* ctx, int on) {
     if (!ctx) return SCX_ERR_VALIDATION;
     ctx->timer.on = on != 0;
