@@ -638,7 +638,8 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     CK(dmalloc(&d.gamma, p));
     CK(dmalloc(&d.trust, p));
     CK(dmalloc(&d.status, d.ntiles));
-    CK(dmalloc(&d.slots, 2 * d.ntiles * 4));
+    CK(dmalloc(&d.slots, 2 * d.ntiles * 8));
+    CK(cudaMemsetAsync(d.slots, 0, 2 * d.ntiles * 8 * sizeof(double), s));
     CK(dmalloc(&d.partial, 2 * d.ntiles));
     CK(dmalloc(&ctx->xdense, d.npad));
     CK(cudaMemsetAsync(d.D, 0, d.npad * sizeof(double), s));
@@ -862,7 +863,8 @@ scx_status scx_segmented_inclusive_scan(scx_ctx* ctx, int64_t n, const double* v
     CK(dmalloc(&t.D, t.npad));
     CK(cudaMalloc(&t.code, t.npad));
     CK(dmalloc(&t.status, t.ntiles));
-    CK(dmalloc(&t.slots, 2 * t.ntiles * 4));
+    CK(dmalloc(&t.slots, 2 * t.ntiles * 8));
+    CK(cudaMemsetAsync(t.slots, 0, 2 * t.ntiles * 8 * sizeof(double), s));
     CK(dmalloc(&t.partial, 2 * t.ntiles));
     CK(dmalloc(&outd, t.npad));
     CK(cudaMemsetAsync(t.D, 0, t.npad * sizeof(double), s));
