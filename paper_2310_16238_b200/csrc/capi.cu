@@ -588,7 +588,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     ctx->event_h.assign(event, event + n);
 
     // --- CSC
-    CK(dmalloc(&ctx->rows_d, nnz));
+    CK(dmalloc(&ctx->rows_d, nnz + 16));  // +16: 16-B-aligned bulk copies may overhang
     CK(dmalloc(&ctx->col_beg_d, p + 1));
     CK(dmalloc(&ctx->val_off_d, p));
     CK(cudaMemcpyAsync(ctx->col_beg_d, col_ptr, (p + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
@@ -610,7 +610,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         cudaFree(stage);
     }
     if (nnz > 0) k_check_rows<<<1184, 256, 0, s>>>(ctx->rows_d, ctx->col_beg_d, p, nnz, n, d.ctl);
-    CK(dmalloc(&ctx->vals_d, compact.size()));
+    CK(dmalloc(&ctx->vals_d, compact.size() + 16));
     if (!compact.empty())
         CK(cudaMemcpyAsync(ctx->vals_d, compact.data(), compact.size() * sizeof(double),
                            cudaMemcpyHostToDevice, s));
