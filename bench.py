@@ -346,7 +346,7 @@ def main():
         e2e_times.append(el)
         e2e_evals.append(r2.n_evaluations)
         dd2.close()
-    e2e_value = float(np.mean(e2e_evals)) / float(np.mean(e2e_times))
+    e2e_value = (float(np.mean(e2e_evals)) / float(np.mean(e2e_times))) if e2e_times else None
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -401,7 +401,8 @@ def main():
                          "k3_in_fit_avg_launch_ms": k3_loop_ms},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "seconds_per_step": float(np.mean(e2e_times))},
+                    "d2h_bytes_per_step": int(d2h),
+                    "seconds_per_step": float(np.mean(e2e_times)) if e2e_times else None},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

@@ -1,0 +1,311 @@
+// Drop-in replacement for the reference's proj/src/likelihood.cpp and
+// proj/src/optimizer.cpp: the same `namespace stratcox` symbols
+// (proj/include/stratcox/likelihood.hpp, optimizer.hpp) implemented over the
+// C-ABI of libstratcox_b200.so (include/stratcox_b200.h).
+//
+// Build it against the reference headers and link it in place of the two
+// reference translation units (oracle/Makefile target
+// `dropin` builds the reference's own acceptance suite this way).
+//
+// Contexts: one scx_ctx per calling thread (thread_local), because the
+// reference calls ccd_fit concurrently from OpenMP threads
+// (proj/src/resample.cpp:121,207). The uploaded design is cached per thread
+// and keyed by the design object's identity (address, storage pointers and
+// shape); a CoefficientState passed by the caller is uploaded per call
+// (parity boundary), while ccd_fit keeps its whole loop on the device.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "stratcox/likelihood.hpp"
+#include "stratcox/optimizer.hpp"
+#include "stratcox_b200.h"
+
+namespace stratcox {
+
+namespace {
+
+struct ThreadCtx {
+    scx_ctx* h = nullptr;
+    const SortedDesign* design = nullptr;
+    const void* time_ptr = nullptr;
+    const void* cols_ptr = nullptr;
+    std::size_t n = 0, p = 0, nnz = 0;
+    ~ThreadCtx() {
+        if (h) scx_destroy(h);
+    }
+};
+
+thread_local ThreadCtx g_ctx;
+
+// Replace the C-ABI's default covariate name "xN" with the design's own.
+std::string with_names(std::string msg, const SortedDesign* d) {
+    const std::string tag = "for covariate x";
+    const auto pos = msg.find(tag);
+    if (d && pos != std::string::npos) {
+        const std::size_t j = std::stoul(msg.substr(pos + tag.size())) - 1;
+        msg = msg.substr(0, pos) + "for covariate " + d->data.covariate_name(j);
+    }
+    return msg;
+}
+
+[[noreturn]] void raise(scx_status s, const std::string& msg) {
+    switch (s) {
+        case SCX_ERR_VALIDATION: throw validation_error(msg);
+        case SCX_ERR_NUMERIC: throw numeric_error(msg);
+        case SCX_ERR_INTERNAL: throw internal_error(msg);
+        default: throw error("CUDA backend: " + msg);
+    }
+}
+
+void check(scx_status s, const SortedDesign* d = nullptr) {
+    if (s != SCX_OK) raise(s, with_names(scx_last_error(g_ctx.h), d));
+}
+
+void check_rule(scx_status s) {
+    if (s != SCX_OK) raise(s, scx_rule_error());
+}
+
+scx_ctx* ctx_for(const SortedDesign& d) {
+    std::size_t nnz = 0;
+    for (const auto& c : d.data.columns) nnz += c.nnz();
+    ThreadCtx& t = g_ctx;
+    if (t.h && t.design == &d && t.time_ptr == d.data.time.data() &&
+        t.cols_ptr == d.data.columns.data() && t.n == d.n_rows() && t.p == d.n_covariates() &&
+        t.nnz == nnz)
+        return t.h;
+    if (!t.h) {
+        if (scx_create(0, &t.h) != SCX_OK) {
+            t.h = nullptr;
+            throw error("CUDA backend: no usable sm_100 device");
+        }
+    }
+    std::vector<int64_t> col_ptr(d.n_covariates() + 1, 0);
+    std::vector<int64_t> rows;
+    std::vector<double> values;
+    rows.reserve(nnz);
+    values.reserve(nnz);
+    for (std::size_t j = 0; j < d.n_covariates(); ++j) {
+        const SparseColumn& c = d.data.columns[j];
+        rows.insert(rows.end(), c.rows.begin(), c.rows.end());
+        values.insert(values.end(), c.values.begin(), c.values.end());
+        col_ptr[j + 1] = static_cast<int64_t>(rows.size());
+    }
+    t.design = nullptr;
+    check(scx_upload_design(t.h, static_cast<int64_t>(d.n_rows()), d.n_strata(),
+                            d.stratum_offsets.data(), d.data.event.data(), d.tie_group_end.data(),
+                            static_cast<int64_t>(d.n_covariates()), col_ptr.data(), rows.data(),
+                            values.data()),
+          &d);
+    t.design = &d;
+    t.time_ptr = d.data.time.data();
+    t.cols_ptr = d.data.columns.data();
+    t.n = d.n_rows();
+    t.p = d.n_covariates();
+    t.nnz = nnz;
+    return t.h;
+}
+
+void put_state(scx_ctx* h, const SortedDesign& d, const CoefficientState& st) {
+    check(scx_set_state(h, st.beta.data(), st.xbeta.data(), st.exp_xbeta.data(),
+                        st.updates_since_refresh),
+          &d);
+}
+
+void get_state(scx_ctx* h, const SortedDesign& d, CoefficientState& st) {
+    st.beta.resize(d.n_covariates());
+    st.xbeta.resize(d.n_rows());
+    st.exp_xbeta.resize(d.n_rows());
+    uint32_t u = 0;
+    check(scx_get_state(h, st.beta.data(), st.xbeta.data(), st.exp_xbeta.data(), &u), &d);
+    st.updates_since_refresh = u;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ likelihood.hpp
+
+CoefficientState make_state(const SortedDesign& design, std::span<const double> beta) {
+    if (beta.size() != design.n_covariates())
+        throw validation_error("beta length does not match covariate count");
+    scx_ctx* h = ctx_for(design);
+    check(scx_make_state(h, beta.data()), &design);
+    CoefficientState st;
+    get_state(h, design, st);
+    st.updates_since_refresh = 0;
+    return st;
+}
+
+void refresh_xbeta(const SortedDesign& design, CoefficientState& state) {
+    scx_ctx* h = ctx_for(design);
+    put_state(h, design, state);
+    check(scx_refresh_xbeta(h), &design);
+    get_state(h, design, state);
+}
+
+void update_xbeta(const SortedDesign& design, CoefficientState& state, std::size_t j,
+                  double delta) {
+    if (j >= design.n_covariates()) throw validation_error("covariate index out of range");
+    if (!std::isfinite(delta)) throw numeric_error("non-finite coordinate step");
+    scx_ctx* h = ctx_for(design);
+    put_state(h, design, state);
+    check(scx_update_xbeta(h, static_cast<int64_t>(j), delta), &design);  // throws: host state untouched
+    get_state(h, design, state);
+}
+
+void ScanWorkspace::resize(std::size_t n) {
+    n1.resize(n);
+    n2.resize(n);
+    scanned_d.resize(n);
+    scanned_n1.resize(n);
+    scanned_n2.resize(n);
+}
+
+double log_partial_likelihood(const SortedDesign& design, const CoefficientState& state,
+                              const ExecutionConfig& config, ScanWorkspace& /*workspace*/,
+                              ScanCounters* /*counters*/) {
+    validate(config);
+    if (state.xbeta.size() != design.n_rows()) throw validation_error("state does not match design");
+    scx_ctx* h = ctx_for(design);
+    put_state(h, design, state);
+    double ll = 0.0;
+    check(scx_log_partial_likelihood(h, &ll), &design);
+    return ll;
+}
+
+double log_partial_likelihood(const SortedDesign& design, const CoefficientState& state,
+                              const ExecutionConfig& config, ScanCounters* counters) {
+    ScanWorkspace ws;
+    return log_partial_likelihood(design, state, config, ws, counters);
+}
+
+GradHess gradient_hessian(const SortedDesign& design, const CoefficientState& state,
+                          std::size_t j, ScanWorkspace& /*workspace*/,
+                          const ExecutionConfig& config, ScanCounters* /*counters*/) {
+    if (j >= design.n_covariates()) throw validation_error("covariate index out of range");
+    if (state.xbeta.size() != design.n_rows()) throw validation_error("state does not match design");
+    validate(config);
+    scx_ctx* h = ctx_for(design);
+    put_state(h, design, state);
+    GradHess out;
+    check(scx_gradient_hessian(h, static_cast<int64_t>(j), &out.gradient, &out.hessian), &design);
+    return out;
+}
+
+GradHess naive_gradient_hessian(const SortedDesign& design, const CoefficientState& state,
+                                std::size_t j) {
+    if (j >= design.n_covariates()) throw validation_error("covariate index out of range");
+    scx_ctx* h = ctx_for(design);
+    put_state(h, design, state);
+    GradHess out;
+    check(scx_naive_gradient_hessian(h, static_cast<int64_t>(j), &out.gradient, &out.hessian),
+          &design);
+    return out;
+}
+
+double naive_log_partial_likelihood(const SortedDesign& design, const CoefficientState& state) {
+    scx_ctx* h = ctx_for(design);
+    put_state(h, design, state);
+    double ll = 0.0;
+    check(scx_naive_log_partial_likelihood(h, &ll), &design);
+    return ll;
+}
+
+// ------------------------------------------------------------------ optimizer.hpp
+
+PenaltySpec PenaltySpec::shared(std::size_t p, double gamma_value,
+                                std::span<const std::size_t> unpenalized) {
+    PenaltySpec spec{std::vector<double>(p, gamma_value)};
+    for (const std::size_t j : unpenalized) {
+        if (j >= p) throw validation_error("unpenalized index out of range");
+        spec.gamma[j] = 0.0;
+    }
+    return spec;
+}
+
+double PenaltySpec::value(std::span<const double> beta) const {
+    double total = 0.0;
+    for (std::size_t j = 0; j < beta.size(); ++j) total += gamma[j] * std::abs(beta[j]);
+    return total;
+}
+
+void PenaltySpec::validate(std::size_t p) const {
+    if (gamma.size() != p) throw validation_error("penalty length does not match covariate count");
+    for (const double g : gamma)
+        if (!std::isfinite(g) || g < 0.0)
+            throw validation_error("penalty weights must be finite and non-negative");
+}
+
+double newton_step(double g1, double g2, bool* flat) {
+    double step = 0.0;
+    int fl = 0;
+    check_rule(scx_newton_step(g1, g2, &step, &fl));
+    if (flat) *flat = fl != 0;
+    return step;
+}
+
+TrustOutcome apply_trust_region(double delta_proposed, double trust) {
+    TrustOutcome out{};
+    check_rule(scx_apply_trust_region(delta_proposed, trust, &out.applied, &out.next_trust));
+    return out;
+}
+
+ProposedStep l1_coordinate_update(double g1, double g2, double beta_j, double gamma_j) {
+    ProposedStep out;
+    int sk = 0, fl = 0;
+    check_rule(scx_l1_coordinate_update(g1, g2, beta_j, gamma_j, &out.step, &sk, &fl));
+    out.skipped = sk != 0;
+    out.flat = fl != 0;
+    return out;
+}
+
+namespace {
+
+FitResult run_fit(const SortedDesign& design, const PenaltySpec& penalty,
+                  const OptimizerConfig& config, const double* initial_beta) {
+    const std::size_t p = design.n_covariates();
+    penalty.validate(p);
+    validate(config.exec);
+    scx_ctx* h = ctx_for(design);
+    FitResult r;
+    r.beta.assign(p, 0.0);
+    r.trust.assign(p, 0.0);
+    std::vector<double> trace(static_cast<std::size_t>(std::max(1, config.max_cycles)) + 1);
+    std::vector<int64_t> warn(64);
+    scx_fit_options opt{config.max_cycles, config.tolerance, config.initial_trust};
+    scx_fit_result out{};
+    out.beta = r.beta.data();
+    out.trust = r.trust.data();
+    out.objective_trace = trace.data();
+    out.warning_coords = warn.data();
+    out.warning_cap = static_cast<int32_t>(warn.size());
+    check(scx_ccd_fit(h, penalty.gamma.data(), &opt, initial_beta, &out), &design);
+    r.objective_trace.assign(trace.begin(), trace.begin() + out.trace_len);
+    r.cycles_used = out.cycles_used;
+    r.converged = out.converged != 0;
+    for (int w = 0; w < out.n_warnings; ++w) {
+        const std::string name =
+            w < out.warning_cap ? design.data.covariate_name(static_cast<std::size_t>(warn[w])) : "?";
+        r.warnings.push_back("coordinate " + name +
+                             " skipped: step overflow persisted after 10 halvings");
+    }
+    return r;
+}
+
+}  // namespace
+
+FitResult ccd_fit(const SortedDesign& design, const PenaltySpec& penalty,
+                  const OptimizerConfig& config) {
+    return run_fit(design, penalty, config, nullptr);
+}
+
+FitResult ccd_fit(const SortedDesign& design, const PenaltySpec& penalty,
+                  const OptimizerConfig& config, std::span<const double> initial_beta) {
+    if (initial_beta.size() != design.n_covariates())
+        throw validation_error("initial beta length does not match covariate count");
+    return run_fit(design, penalty, config, initial_beta.data());
+}
+
+}  // namespace stratcox
