@@ -1,5 +1,5 @@
-// Drop-in replacement for the reference's proj/src/likelihood.cpp and
-// proj/src/optimizer.cpp: the same `namespace stratcox` symbols
+// Drop-in replacement for the reference's proj/src/likelihood.cpp,
+// proj/src/optimizer.cpp and proj/src/scan.cpp: the same `namespace stratcox` symbols
 // (proj/include/stratcox/likelihood.hpp, optimizer.hpp) implemented over the
 // C-ABI of libstratcox_b200.so (include/stratcox_b200.h).
 //
@@ -13,14 +13,20 @@
 // and keyed by the design object's identity (address, storage pointers and
 // shape); a CoefficientState passed by the caller is uploaded per call
 // (parity boundary), while ccd_fit keeps its whole loop on the device.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 #include "stratcox/likelihood.hpp"
 #include "stratcox/optimizer.hpp"
+#include "stratcox/scan.hpp"
 #include "stratcox_b200.h"
 
 namespace stratcox {
@@ -124,6 +130,88 @@ void get_state(scx_ctx* h, const SortedDesign& d, CoefficientState& st) {
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------ scan.hpp
+// Replaces proj/src/scan.cpp: the scans run on the device (same flag-value
+// tile scan as the likelihood kernels); the chunk-runner and config helpers
+// stay host utilities.
+
+int default_worker_count() {
+#ifdef _OPENMP
+    return std::max(1, omp_get_max_threads());
+#else
+    return 1;
+#endif
+}
+
+void validate(const ExecutionConfig& config) {
+    if (config.chunk_size < 1) throw validation_error("chunk_size must be >= 1");
+    if (config.worker_count < 1) throw validation_error("worker_count must be >= 1");
+}
+
+namespace detail {
+void run_chunks(const ChunkPlan& plan, int worker_count, void* ctx,
+                void (*body)(void*, std::int64_t)) {
+    (void)worker_count;
+    for (std::int64_t c = 0; c < plan.count; ++c) body(ctx, c);
+}
+}  // namespace detail
+
+namespace {
+scx_ctx* scan_ctx() {
+    ThreadCtx& t = g_ctx;
+    if (!t.h && scx_create(0, &t.h) != SCX_OK) {
+        t.h = nullptr;
+        throw error("CUDA backend: no usable sm_100 device");
+    }
+    return t.h;
+}
+}  // namespace
+
+void segmented_inclusive_scan(std::span<const double> values, std::span<const std::uint8_t> flags,
+                              std::span<double> out, const ExecutionConfig& config,
+                              ScanCounters* counters) {
+    if (values.empty()) throw validation_error("empty scan input");
+    if (flags.size() != values.size())
+        throw validation_error("values and flags must have equal length");
+    if (out.size() != values.size()) throw validation_error("scan output size mismatch");
+    if (!flags[0]) throw validation_error("first element must head a segment");
+    validate(config);
+    check(scx_segmented_inclusive_scan(scan_ctx(), static_cast<int64_t>(values.size()),
+                                       values.data(), flags.data(), out.data()));
+    if (counters) counters->elements.fetch_add(values.size(), std::memory_order_relaxed);
+}
+
+std::vector<double> segmented_inclusive_scan(std::span<const double> values,
+                                             std::span<const std::uint8_t> flags,
+                                             const ExecutionConfig& config,
+                                             ScanCounters* counters) {
+    std::vector<double> out(values.size());
+    segmented_inclusive_scan(values, flags, out, config, counters);
+    return out;
+}
+
+void inclusive_scan(std::span<const double> values, std::span<double> out,
+                    const ExecutionConfig& config, ScanCounters* counters) {
+    if (values.empty()) throw validation_error("empty scan input");
+    if (out.size() != values.size()) throw validation_error("scan output size mismatch");
+    std::vector<std::uint8_t> flags(values.size(), 0);
+    flags[0] = 1;
+    segmented_inclusive_scan(values, flags, out, config, counters);
+}
+
+std::vector<double> inclusive_scan(std::span<const double> values, const ExecutionConfig& config,
+                                   ScanCounters* counters) {
+    std::vector<double> out(values.size());
+    inclusive_scan(values, out, config, counters);
+    return out;
+}
+
+double chunked_sum(std::span<const double> values, const ExecutionConfig& config,
+                   ScanCounters* counters) {
+    return chunked_transform_sum(
+        values.size(), [&](std::size_t i) { return values[i]; }, config, counters);
+}
 
 // ------------------------------------------------------------------ likelihood.hpp
 

@@ -29,7 +29,7 @@ constexpr int kTileRows = 4096;
 constexpr int kThreads = 256;
 constexpr int kRowsPerThread = kTileRows / kThreads;  // 16
 constexpr int kWarps = kThreads / 32;
-constexpr int kLookbackWindows = 4;  // smem stack depth of the look-back
+constexpr int kLookbackWindows = 16;  // smem stack depth of the look-back (512 tiles)
 
 // look-back slot states (low 2 bits of the status word; high 30 bits = epoch)
 constexpr uint32_t kStAgg = 1;

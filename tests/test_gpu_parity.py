@@ -273,6 +273,7 @@ def _compare_all(oracle, a, beta, values=True, tol=GH_RTOL):
     (20000, 20000, 2, 0.3, 8),  # every row its own stratum: all heads
     (50000, 997, 3, 0.05, 1e6), # many strata, nearly no ties
     (70000, 2, 2, 0.01, 2),     # two time values: tie groups of ~17k rows (u16 codes)
+    (3_000_000, 1, 2, 0.01, 1e9),  # one stratum over 733 tiles: deepest look-backs
 ])
 def test_edge_shapes_vs_oracle(oracle, ref, n, strata, p, density, grid):
     ds = ref.random_dataset(1000 + n + strata, n, strata, p, density, grid)
