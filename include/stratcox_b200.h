@@ -164,6 +164,16 @@ scx_status scx_timing_reset(scx_ctx* ctx);
 /* kind: 0 = fused scan+reduce (K1), 1 = update (K3), 2 = log-likelihood (K2) */
 scx_status scx_timing_get(scx_ctx* ctx, int kind, double* total_ms, int64_t* launches);
 
+/* Fused scan+reduce decomposition: 0 = automatic (stratum-aligned chunk per
+ * CTA when the strata are small enough, else cross-CTA look-back), 1 = always
+ * look-back, 2 = chunks when available. *chunked (may be NULL) receives
+ * whether the chunked kernel will run. Results agree within rounding. */
+scx_status scx_set_k1_mode(scx_ctx* ctx, int mode, int* chunked);
+
+/* Profiling: per-event clock64 trace of the last fused scan+reduce launch made
+ * with SCX_K1_DBG bit 8 set (CTAs 0 and 73, tiles < 511): out[2][512][8]. */
+scx_status scx_debug_k1_trace(long long* out);
+
 /* Number of kernels this context has launched so far (bench bookkeeping). */
 int64_t scx_launch_count(const scx_ctx* ctx);
 

@@ -78,6 +78,8 @@ SIGNATURES = {
     "scx_timing_get": (C.c_int, [_vp, C.c_int, _dp, _i64p]),
     "scx_stream": (_vp, [_vp]),
     "scx_launch_count": (C.c_int64, [_vp]),
+    "scx_debug_k1_trace": (C.c_int, [_i64p]),
+    "scx_set_k1_mode": (C.c_int, [_vp, C.c_int, _ip]),
     "scx_comm_unique_id": (C.c_int, [C.c_char_p]),
     "scx_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
     "scx_comm_destroy": (C.c_int, [_vp]),

@@ -69,13 +69,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     return fn;
 }
 
-// [npad/16][16] f64 view, box 16 x 256 (one 4096-row tile), 128-B swizzle.
-bool make_tmap(CUtensorMap* m, double* base, int64_t npad) {
+// [npad/16][16] f64 view, box 16 x (tile_rows/16) (one tile), 128-B swizzle.
+bool make_tmap(CUtensorMap* m, double* base, int64_t npad, int tile_rows = kTileRows) {
     auto enc = tmap_encoder();
     if (!enc) return false;
     cuuint64_t dims[2] = {16, (cuuint64_t)(npad / 16)};
     cuuint64_t strides[1] = {16 * sizeof(double)};
-    cuuint32_t box[2] = {16, 256};
+    cuuint32_t box[2] = {16, (cuuint32_t)(tile_rows / 16)};
     cuuint32_t es[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -159,7 +159,8 @@ void free_design(scx_ctx* ctx) {
     void* ptrs[] = {d.code,   d.D,          d.eta,         d.beta,      d.gamma,
                     d.trust,  d.status,     d.slots,       d.partial,   ctx->xdense,
                     ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
-                    ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d};
+                    ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d, d.lasth1,
+                    d.chunk_rows};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     const DevCtl* keep_ctl = d.ctl;
@@ -558,6 +559,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     d.p = p;
     d.ntiles = (n + kTileRows - 1) / kTileRows;
     d.npad = d.ntiles * kTileRows;
+    d.ntiles1 = d.npad / kK1TileRows;
     cudaStream_t s = ctx->stream;
 
     // --- event codes
@@ -580,7 +582,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     unsigned int maxw = 0;
     CK(cudaMemcpyAsync(&maxw, maxw_d, sizeof maxw, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    d.code_bytes = maxw <= 0x3fu ? 1 : (maxw <= 0x3fffu ? 2 : 4);
+    d.code_bytes = maxw <= 0x1fu ? 1 : (maxw <= 0x1fffu ? 2 : 4);
     CK(cudaMalloc(&d.code, d.npad * d.code_bytes));
     KL(1, launch_build_codes(d.code, d.code_bytes, n, d.npad, event_d, tie_d, ctx->offsets_d, k, w_d,
                           s));
@@ -622,8 +624,8 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     std::vector<ColStats> stats(p);
     if (p > 0)
         CK(cudaMemcpyAsync(stats.data(), stats_d, p * sizeof(ColStats), cudaMemcpyDeviceToHost, s));
-    CK(dmalloc(&ctx->tptr_d, p * (d.ntiles + 1)));
-    if (p > 0) KL(1, launch_tile_ptr(ctx->tptr_d, ctx->rows_d, ctx->col_beg_d, p, d.ntiles, s));
+    CK(dmalloc(&ctx->tptr_d, p * (d.ntiles1 + 1)));
+    if (p > 0) KL(1, launch_tile_ptr(ctx->tptr_d, ctx->rows_d, ctx->col_beg_d, p, d.ntiles1, s));
     CK(cudaStreamSynchronize(s));
     cudaFree(event_d);
     cudaFree(tie_d);
@@ -637,9 +639,47 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     CK(dmalloc(&d.beta, p));
     CK(dmalloc(&d.gamma, p));
     CK(dmalloc(&d.trust, p));
+    CK(dmalloc(&d.lasth1, d.ntiles1));
+    KL(1, launch_last_head(d.lasth1, ctx->offsets_d, k, d.ntiles1, s));
+    // Stratum-aligned chunks, one per SM, for the chunked fused scan: strata
+    // are assigned in order, a chunk closing once it reaches its share of
+    // the remaining rows. Used when the largest stratum is at most a quarter
+    // of a chunk (so the longest chunk exceeds n/G by <= 25%); otherwise the
+    // fused scan uses the cross-CTA look-back.
+    {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        const int64_t G = sms > 0 ? sms : 148;
+        int64_t maxk = 0;
+        for (int32_t q = 0; q < k; ++q) maxk = std::max<int64_t>(maxk, offsets[q + 1] - offsets[q]);
+        bool ok = k >= 2 * G && n >= G * 4 * (int64_t)kK1TileRows && 4 * maxk <= n / G;
+        std::vector<int32_t> ch;
+        if (ok) {
+            ch.push_back(0);
+            int32_t q = 0;
+            for (int64_t c = 1; c < G && ok; ++c) {
+                const int64_t target = ch.back() + (n - ch.back()) / (G - c + 1);
+                while (q < k && offsets[q + 1] <= target) ++q;
+                // close at the head nearest to the target
+                int64_t h = offsets[q];
+                if (q + 1 <= k && offsets[q + 1] - target < target - h) h = offsets[q + 1];
+                if (h <= ch.back() || h >= n) ok = false;
+                else ch.push_back((int32_t)h);
+            }
+            ch.push_back((int32_t)n);
+        }
+        d.chunk_rows = nullptr;
+        d.nchunks = 0;
+        if (ok) {
+            CK(dmalloc(&d.chunk_rows, ch.size()));
+            CK(cudaMemcpyAsync(d.chunk_rows, ch.data(), ch.size() * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, s));
+            d.nchunks = (int32_t)G;
+        }
+    }
     CK(dmalloc(&d.status, d.ntiles));
-    CK(dmalloc(&d.slots, 2 * d.ntiles * 8));
-    CK(cudaMemsetAsync(d.slots, 0, 2 * d.ntiles * 8 * sizeof(double), s));
+    CK(dmalloc(&d.slots, 2 * d.ntiles1 * 8));
+    CK(cudaMemsetAsync(d.slots, 0, 2 * d.ntiles1 * 8 * sizeof(double), s));
     CK(dmalloc(&d.partial, 2 * d.ntiles));
     CK(dmalloc(&ctx->xdense, d.npad));
     CK(cudaMemsetAsync(d.D, 0, d.npad * sizeof(double), s));
@@ -653,7 +693,8 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     d.col_beg = ctx->col_beg_d;
     d.val_off = ctx->val_off_d;
     d.offsets = ctx->offsets_d;
-    if (!make_tmap(&d.tmap_D, d.D, d.npad) || !make_tmap(&d.tmap_eta, d.eta, d.npad))
+    if (!make_tmap(&d.tmap_D, d.D, d.npad) || !make_tmap(&d.tmap_eta, d.eta, d.npad) ||
+        !make_tmap(&d.tmap_D1, d.D, d.npad, kK1TileRows))
         return fail(ctx, SCX_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 
     // co-resident block count for the cooperative kernels
@@ -1136,6 +1177,17 @@ scx_status scx_gamma_max(scx_ctx* ctx, const double* gamma_template, double* out
 }
 
 // ---------------------------------------------------------------- timing
+scx_status scx_set_k1_mode(scx_ctx* ctx, int mode, int* chunked) {
+    if (!ctx || mode < 0 || mode > 2) return SCX_ERR_VALIDATION;
+    ctx->d.k1_mode = mode;
+    if (chunked) *chunked = (ctx->d.chunk_rows != nullptr && mode != 1) ? 1 : 0;
+    return SCX_OK;
+}
+
+scx_status scx_debug_k1_trace(long long* out) {
+    return k1_trace_copy(out) == cudaSuccess ? SCX_OK : SCX_ERR_CUDA;
+}
+
 int64_t scx_launch_count(const scx_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 scx_status scx_timing_enable(scx_ctx* ctx, int on) {

@@ -12,7 +12,7 @@
 //           ends turns the gather into a forward stream (exact algebra).
 //   rows    i32[nnz]   CSC row indices, columns concatenated (SparseColumn::rows)
 //   vals    f64[nval]  values of non-indicator columns only, compacted
-//   tptr    i32[p][ntiles+1]  per column, entry offset of each tile's first row
+//   tptr    i32[p][ntiles1+1] per column, entry offset of each 2048-row K1 tile's first row
 //   beta, gamma, trust  f64[p]
 #pragma once
 
@@ -26,6 +26,7 @@
 namespace scx {
 
 constexpr int kTileRows = 4096;
+constexpr int kK1TileRows = 2048;  // fused scan+reduce (K1) tile
 constexpr int kThreads = 256;
 constexpr int kRowsPerThread = kTileRows / kThreads;  // 16
 constexpr int kWarps = kThreads / 32;
@@ -127,6 +128,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+// Same wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (used by the producer / look-back warps, which would
+// otherwise spin and take issue slots from the compute warps).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -195,6 +210,7 @@ struct DesignDev {
     int64_t n;
     int64_t npad;
     int64_t ntiles;
+    int64_t ntiles1;          // K1 tiles (kK1TileRows)
     int64_t p;
     int32_t k;
     int32_t code_bytes;
@@ -204,6 +220,10 @@ struct DesignDev {
     const int32_t* rows;
     const double* vals;
     const int32_t* tptr;
+    int32_t* lasth1;          // [ntiles1] last stratum head offset in each K1 tile (-1: none)
+    int32_t* chunk_rows;      // [nchunks+1] stratum-aligned chunk starts (NULL: look-back mode)
+    int32_t nchunks;
+    int32_t k1_mode;          // 0 auto, 1 force look-back, 2 chunk when available
     const int64_t* col_beg;   // [p+1]
     const int64_t* val_off;   // [p] (-1 indicator)
     const int64_t* offsets;   // [k+1]
@@ -215,7 +235,8 @@ struct DesignDev {
     double* slots;            // [2][ntiles][4] agg / inc (s0, s1, s2, flag)
     double* partial;          // [ntiles][2]
     DevCtl* ctl;
-    CUtensorMap tmap_D;
+    CUtensorMap tmap_D;       // box 16 x 256 (4096-row tile)
+    CUtensorMap tmap_D1;      // box 16 x 128 (2048-row K1 tile)
     CUtensorMap tmap_eta;
     int coop_blocks;          // co-resident blocks for the cooperative kernels
 };
@@ -223,6 +244,7 @@ struct DesignDev {
 enum K1Mode : int { kK1Eval = 0, kK1Fit = 1, kK1Diag = 2, kK1Partial = 3 };
 
 cudaError_t launch_k1(const DesignDev& d, const ColArgs& col, int mode, cudaStream_t s);
+cudaError_t k1_trace_copy(long long* out);  // [2][512][8] clock64 (SCX_K1_DBG bit 8)
 cudaError_t launch_k2(const DesignDev& d, int fit_mode, cudaStream_t s);
 // K3: apply the step decided by K1 (mode 0 = fit with halving, 1 = standalone
 // update_xbeta with delta given, no halving -> "step overflow")
@@ -246,6 +268,8 @@ cudaError_t launch_tie_weights(uint32_t* w, const uint8_t* event, const int64_t*
                                DevCtl* ctl, unsigned int* maxw, cudaStream_t s);
 cudaError_t launch_tile_ptr(int32_t* tptr, const int32_t* rows, const int64_t* col_beg,
                             int64_t p, int64_t ntiles, cudaStream_t s);
+cudaError_t launch_last_head(int32_t* lasth, const int64_t* offsets, int32_t k, int64_t ntiles1,
+                             cudaStream_t s);
 cudaError_t launch_narrow_rows(int32_t* dst, const int64_t* src, int64_t count, cudaStream_t s);
 cudaError_t launch_scan_primitive(const DesignDev& d, double* out, cudaStream_t s);
 cudaError_t launch_k3_sharded(const DesignDev& d, const ColArgs& col, cudaStream_t s);

@@ -351,3 +351,66 @@ def test_large_n_gradient_vs_oracle(oracle, ref, n, k, p):
     g1 = sx.gradient_hessian(dd, st, 0)
     g2 = sx.gradient_hessian(dd, st, 0)
     assert (g1.gradient, g1.hessian) == (g2.gradient, g2.hessian)
+
+
+# ---------------------------------------------------------------- fused-scan decompositions
+def _k1_mode(dd, mode):
+    """0 auto / 1 cross-CTA look-back / 2 stratum-aligned chunks; returns 1 if chunked."""
+    import ctypes as C
+    from paper_2310_16238_b200 import _capi
+    ch = C.c_int()
+    assert _capi.load().scx_set_k1_mode(dd.handle, mode, C.byref(ch)) == 0
+    return ch.value
+
+
+@pytest.mark.parametrize("n,k,p,density,grid,values", [
+    (1_500_000, 1500, 4, 0.02, 1e9, False),  # indicators, continuous times: fast path
+    (1_300_000, 2000, 3, 0.15, 1e9, True),   # value columns, > 64 entries per quarter
+    (1_400_000, 1500, 3, 0.01, 40, True),    # heavy ties (general path, wide codes)
+    (1_250_000, 20000, 2, 0.05, 1e9, False),  # small strata: heads in most threads' rows
+])
+def test_chunked_and_lookback_match_oracle(oracle, ref, n, k, p, density, grid, values):
+    """The stratum-aligned chunk kernel and the look-back kernel both agree with
+    the oracle (1e-10) and are each bitwise reproducible."""
+    if values:  # real-valued X (oracles::random_dataset)
+        ds = ref.random_dataset(31 + n + k, n, k, p, density, grid)
+        a = oracle.build_sorted_design(ds)
+    else:       # binary X (simulate.cpp): indicator columns
+        ds = ref.simulate(n, p, density, 0.5, k, 0.3, 31 + k)
+        h0, a = ref.build_design(ds)
+        ref.free_design(h0)
+    d = oracle.design(a)
+    dd = upload(a, values=values)
+    assert _k1_mode(dd, 0) == 1, "design expected to take the chunked kernel"
+    rng = np.random.default_rng(k)
+    beta = rng.normal(0, 0.3, p)
+    st = sx.make_state(dd, beta)
+    xb, ex = oracle.make_state(d, beta)
+    for j in range(p):
+        g, h = oracle.gradient_hessian(d, ex, j)
+        for mode in (2, 1):
+            _k1_mode(dd, mode)
+            r1 = sx.gradient_hessian(dd, st, j)
+            r2 = sx.gradient_hessian(dd, st, j)
+            assert (r1.gradient, r1.hessian) == (r2.gradient, r2.hessian), (j, mode)
+            assert G.close_rel(r1.gradient, g, GH_RTOL), (j, mode, r1.gradient, g)
+            assert G.close_rel(r1.hessian, h, GH_RTOL), (j, mode, r1.hessian, h)
+    _k1_mode(dd, 0)
+
+
+def test_chunked_fit_matches_oracle(oracle, ref):
+    """A full L1 CCD fit through the chunked kernel against the oracle's fit."""
+    n, k, p = 1_300_000, 1300, 4
+    ds = ref.simulate(n, p, 0.05, 0.5, k, 0.3, 5)
+    h, a = ref.build_design(ds)
+    ref.free_design(h)
+    d = oracle.design(a)
+    dd = upload(a, values=False)
+    assert _k1_mode(dd, 0) == 1
+    gmax = sx.gamma_max(dd)
+    gamma = np.full(p, 0.1 * gmax)
+    want = oracle.ccd_fit(d, gamma, max_cycles=50, tol=1e-8)
+    r = sx.ccd_fit(dd, sx.PenaltySpec(gamma), sx.OptimizerConfig(max_cycles=50, tolerance=1e-8))
+    assert r.cycles_used == want["cycles"]
+    assert np.max(np.abs(r.beta - want["beta"])) <= BETA_ATOL
+    assert np.allclose(r.objective_trace, want["trace"], rtol=LL_RTOL, atol=0)
