@@ -253,8 +253,9 @@ def main():
     for _ in range(args.warmup):
         flush_l2(l2buf)
         r = sx.ccd_fit(dd, pen, cfg)
-    log(f"[bench] warm-up fit: cycles={r.cycles_used} converged={r.converged} "
-        f"nonzero={int(np.count_nonzero(r.beta))} evals={r.n_evaluations}")
+    if args.warmup:
+        log(f"[bench] warm-up fit: cycles={r.cycles_used} converged={r.converged} "
+            f"nonzero={int(np.count_nonzero(r.beta))} evals={r.n_evaluations}")
 
     # ---- timed fits (design resident)
     times, evals, cycles = [], [], []
