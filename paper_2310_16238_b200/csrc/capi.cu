@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
@@ -122,6 +123,11 @@ struct scx_ctx {
     int32_t* rows_d = nullptr;
     double* vals_d = nullptr;
     int32_t* tptr_d = nullptr;
+    // CCD cycle kernel: the nnz > 0 columns in ascending j (device copy) and
+    // their maximal runs of one kind (indicator / value): {first, count, indicator}
+    ColArgs* cols_d = nullptr;
+    std::vector<std::array<int32_t, 3>> runs;
+    bool per_coordinate_fit = false;  // SCX_FIT_PER_COORD=1: one K1 + K3 launch per coordinate
     // multi-GPU
     void* comm = nullptr;
     int nranks = 1, rank = 0;
@@ -160,7 +166,7 @@ void free_design(scx_ctx* ctx) {
                     d.trust,  d.status,     d.slots,       d.partial,   ctx->xdense,
                     ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
                     ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d, d.lasth1,
-                    d.chunk_rows};
+                    d.chunk_rows, ctx->cols_d};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     const DevCtl* keep_ctl = d.ctl;
@@ -175,6 +181,8 @@ void free_design(scx_ctx* ctx) {
     ctx->tptr_d = nullptr;
     ctx->zero_cols_d = nullptr;
     ctx->parts_d = nullptr;
+    ctx->cols_d = nullptr;
+    ctx->runs.clear();
     ctx->cols.clear();
     ctx->zero_cols.clear();
     ctx->has_design = false;
@@ -456,10 +464,12 @@ int scx_device_count(void) {
 }
 
 scx_status scx_create(int device, scx_ctx** out) {
+    static const bool per_coord = getenv("SCX_FIT_PER_COORD") && atoi(getenv("SCX_FIT_PER_COORD"));
     if (!out) return SCX_ERR_VALIDATION;
     *out = nullptr;
     auto* ctx = new scx_ctx();
     ctx->device = device;
+    ctx->per_coordinate_fit = per_coord;
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
         delete ctx;
@@ -680,7 +690,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     CK(dmalloc(&d.status, d.ntiles));
     CK(dmalloc(&d.slots, 2 * d.ntiles1 * 8));
     CK(cudaMemsetAsync(d.slots, 0, 2 * d.ntiles1 * 8 * sizeof(double), s));
-    CK(dmalloc(&d.partial, 2 * d.ntiles));
+    CK(dmalloc(&d.partial, std::max<int64_t>(2 * d.ntiles, 4 * std::max<int64_t>(d.ntiles1, 1024))));
     CK(dmalloc(&ctx->xdense, d.npad));
     CK(cudaMemsetAsync(d.D, 0, d.npad * sizeof(double), s));
     CK(cudaMemsetAsync(d.eta, 0, d.npad * sizeof(double), s));
@@ -720,6 +730,22 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         c.indicator = val_off[j] < 0 ? 1 : 0;
         ctx->cols[j] = c;
         if (c.nnz == 0) ctx->zero_cols.push_back((int32_t)j);
+    }
+    {
+        std::vector<ColArgs> nz;
+        for (int64_t j = 0; j < p; ++j)
+            if (ctx->cols[j].nnz > 0) {
+                const int32_t ind = ctx->cols[j].indicator;
+                if (ctx->runs.empty() || ctx->runs.back()[2] != ind)
+                    ctx->runs.push_back({(int32_t)nz.size(), 0, ind});
+                ctx->runs.back()[1] += 1;
+                nz.push_back(ctx->cols[j]);
+            }
+        CK(dmalloc(&ctx->cols_d, nz.size()));
+        if (!nz.empty())
+            CK(cudaMemcpyAsync(ctx->cols_d, nz.data(), nz.size() * sizeof(ColArgs),
+                               cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
     }
     CK(dmalloc(&ctx->zero_cols_d, ctx->zero_cols.size()));
     if (!ctx->zero_cols.empty())
@@ -1121,10 +1147,20 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
     const double zero = 0.0;
     for (int cycle = 1; cycle <= opt->max_cycles; ++cycle) {
         CK(cudaMemcpyAsync(&d.ctl->max_step, &zero, sizeof zero, cudaMemcpyHostToDevice, s));
-        for (int64_t j = 0; j < p; ++j) {
-            const ColArgs& col = ctx->cols[j];
-            if (col.nnz == 0) continue;
-            if (scx_status st = run_coordinate(ctx, col)) return st;
+        if (ctx->nranks == 1 && !ctx->per_coordinate_fit) {
+            // the whole cycle on the device: one cooperative launch per run of
+            // same-kind columns (one launch for an all-indicator design)
+            for (const auto& run : ctx->runs) {
+                tmark(ctx, 0);
+                KL(1, launch_cycle(d, ctx->cols_d + run[0], run[1], run[2] != 0, s));
+                tend(ctx);
+            }
+        } else {
+            for (int64_t j = 0; j < p; ++j) {
+                const ColArgs& col = ctx->cols[j];
+                if (col.nnz == 0) continue;
+                if (scx_status st = run_coordinate(ctx, col)) return st;
+            }
         }
         if (scx_status st = run_cycle_tail(ctx, true, &ll, &pen, &max_step)) return st;
         tcollect(ctx);

@@ -244,7 +244,11 @@ struct DesignDev {
 enum K1Mode : int { kK1Eval = 0, kK1Fit = 1, kK1Diag = 2, kK1Partial = 3 };
 
 cudaError_t launch_k1(const DesignDev& d, const ColArgs& col, int mode, cudaStream_t s);
-cudaError_t k1_trace_copy(long long* out);  // [2][512][8] clock64 (SCX_K1_DBG bit 8)
+cudaError_t k1_trace_copy(long long* out);
+// one CCD cycle in one cooperative launch over cols_d[0..ncols) (all of one
+// kind: indicator or value columns)
+cudaError_t launch_cycle(const DesignDev& d, const ColArgs* cols_d, int ncols, bool indicator,
+                         cudaStream_t s);  // [2][512][8] clock64 (SCX_K1_DBG bit 8)
 cudaError_t launch_k2(const DesignDev& d, int fit_mode, cudaStream_t s);
 // K3: apply the step decided by K1 (mode 0 = fit with halving, 1 = standalone
 // update_xbeta with delta given, no halving -> "step overflow")
