@@ -29,7 +29,11 @@ $(OBJDIR)/capi.o: $(CSRC)/capi.cu $(CSRC)/internal.cuh $(CSRC)/rules.cuh include
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/capi.ptxas.txt || (cat $(OBJDIR)/capi.ptxas.txt; exit 1)
 
-$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o
+$(OBJDIR)/cv.o: $(CSRC)/cv.cu include/stratcox_b200.h
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/cv.ptxas.txt || (cat $(OBJDIR)/cv.ptxas.txt; exit 1)
+
+$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
 oracle:

@@ -155,6 +155,60 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
  * gamma_template[p] (NULL = every coefficient penalized). */
 scx_status scx_gamma_max(scx_ctx* ctx, const double* gamma_template, double* out);
 
+/* ---------------------------------------------------------------- data sets, path and CV
+ * SurvivalDataset (data.hpp:31-45) in INPUT row order, for the drivers below. */
+typedef struct {
+    int64_t n_rows;
+    const double* time;       /* [n] observed time, >= 0 */
+    const uint8_t* event;     /* [n] 1 event, 0 censored */
+    const int32_t* stratum;   /* [n] dense labels 1..K */
+    const int64_t* subject;   /* [n] originating subject, or NULL (row + 1) */
+    int64_t n_covariates;
+    const int64_t* col_ptr;   /* [p+1] */
+    const int64_t* row_idx;   /* [nnz] input rows, strictly increasing per column */
+    const double* values;     /* [nnz] or NULL (every value 1.0) */
+} scx_dataset;
+
+/* build_sorted_design (data.cpp:68-147: stable sort by stratum ascending,
+ * time descending; CSC re-index; heads; tie-group ends) on the host, then
+ * upload (as scx_upload_design). perm_out [n] may be NULL: sorted row s is
+ * input row perm_out[s]. */
+scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, int64_t* perm_out);
+
+/* default_gamma_grid (resample.hpp:42, resample.cpp:57-68): `size` values
+ * log-spaced over [gamma_max / 1e4, gamma_max]. */
+scx_status scx_default_gamma_grid(double gamma_max, int64_t size, double* out);
+
+/* fold_assignment (resample.hpp:45, resample.cpp:70-91): subjects shuffled by
+ * mt19937_64(seed) and dealt round-robin; fold_of_row [n]. */
+scx_status scx_fold_assignment(const scx_dataset* data, int folds, uint64_t seed,
+                               int32_t* fold_of_row);
+
+typedef struct {               /* CvConfig (resample.hpp:15-19) */
+    int folds;
+    const double* gamma_grid;  /* strictly increasing, positive */
+    int64_t grid_size;
+    uint64_t seed;
+} scx_cv_config;
+
+typedef struct {               /* CvResult (resample.hpp:21-27) */
+    double gamma_star;
+    double* fold_scores;       /* [grid_size][folds] caller-allocated (may be NULL) */
+    double* mean_scores;       /* [grid_size] caller-allocated (may be NULL) */
+    int32_t n_warnings;        /* fits / scores that failed (score -inf) */
+} scx_cv_result;
+
+/* kfold_select_gamma (resample.hpp:53-54, resample.cpp:93-172): per fold, the
+ * warm-started gamma path from the sparse end on the training folds with
+ * held-out partial-likelihood scoring; fits and scores run on the device.
+ * Folds are dealt round-robin over devices[0..n_devices) (NULL/0: device 0),
+ * one host thread per device. error_out (cap bytes, may be NULL) receives the
+ * error message, or the fold warnings one per line on success. */
+scx_status scx_kfold_select_gamma(const scx_dataset* data, const double* penalty_template,
+                                  const scx_cv_config* cv, const scx_fit_options* options,
+                                  const int* devices, int n_devices, scx_cv_result* result,
+                                  char* error_out, int error_cap);
+
 /* ---------------------------------------------------------------- measurement
  * Device time of the kernels launched by the last call, for bench/roofline:
  * per-kernel-class accumulated milliseconds and launch counts since the last

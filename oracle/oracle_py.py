@@ -108,6 +108,12 @@ class Ref:
             "ref_default_gamma_grid": (C.c_int, [C.c_double, C.c_int64, _d]),
             "ref_time_iterations": (C.c_int, [_vp, C.c_double, C.c_int, C.c_int, C.c_int, _d]),
             "ref_time_fit": (C.c_int, [_vp, C.c_double, C.c_int, C.c_double, C.c_int, _d, _ip]),
+            "ref_dataset_subject": (None, [_vp, _i64]),
+            "ref_dataset_set_subject": (None, [_vp, _i64]),
+            "ref_fold_assignment": (C.c_int, [_vp, C.c_int, C.c_uint64, _i32]),
+            "ref_kfold_select_gamma": (C.c_int, [_vp, _d, C.c_int, _d, C.c_int64, C.c_uint64,
+                                                 C.c_int, C.c_double, C.c_double, C.c_int, _d,
+                                                 _d, _d, _ip]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -284,6 +290,47 @@ class Ref:
 
     def max_threads(self):
         return self.L.ref_max_threads()
+
+
+def _ref_resample_methods():
+    def fold_assignment(self, ds, folds, seed, subject=None):
+        """fold_assignment (resample.cpp:70-91) of the reference."""
+        h = self.dataset_handle(ds)
+        try:
+            if subject is not None:
+                sj = np.ascontiguousarray(subject, np.int64)
+                self.L.ref_dataset_set_subject(h, _p(sj, C.c_int64))
+            out = np.empty(ds.n, np.int32)
+            self._chk(self.L.ref_fold_assignment(h, int(folds), int(seed), _p(out, C.c_int32)))
+            return out
+        finally:
+            self.L.ref_dataset_free(h)
+
+    def kfold_select_gamma(self, ds, template, folds, grid, seed, max_cycles=1000, tol=1e-6,
+                           initial_trust=1.0, workers=0, subject=None):
+        """kfold_select_gamma (resample.cpp:93-172) of the reference."""
+        h = self.dataset_handle(ds)
+        try:
+            if subject is not None:
+                sj = np.ascontiguousarray(subject, np.int64)
+                self.L.ref_dataset_set_subject(h, _p(sj, C.c_int64))
+            g = np.ascontiguousarray(grid, np.float64)
+            t = np.ascontiguousarray(template, np.float64)
+            fs = np.empty((g.shape[0], folds)); ms = np.empty(g.shape[0])
+            gs = C.c_double(); nw = C.c_int()
+            self._chk(self.L.ref_kfold_select_gamma(
+                h, _p(t, C.c_double), int(folds), _p(g, C.c_double), g.shape[0], int(seed),
+                int(max_cycles), float(tol), float(initial_trust), int(workers),
+                _p(fs, C.c_double), _p(ms, C.c_double), C.byref(gs), C.byref(nw)))
+            return dict(gamma_star=gs.value, fold_scores=fs, mean_scores=ms, n_warnings=nw.value)
+        finally:
+            self.L.ref_dataset_free(h)
+
+    Ref.fold_assignment = fold_assignment
+    Ref.kfold_select_gamma = kfold_select_gamma
+
+
+_ref_resample_methods()
 
 
 class OrcDesign(C.Structure):

@@ -175,6 +175,51 @@ void ref_dataset_copy(void* h, double* time, uint8_t* event, int32_t* stratum, i
 
 void ref_dataset_free(void* h) { delete static_cast<Dataset*>(h); }
 
+void ref_dataset_subject(void* h, int64_t* out) {
+    const auto& d = static_cast<Dataset*>(h)->data;
+    std::memcpy(out, d.subject.data(), d.subject.size() * sizeof(int64_t));
+}
+
+void ref_dataset_set_subject(void* h, const int64_t* subject) {
+    auto& d = static_cast<Dataset*>(h)->data;
+    d.subject.assign(subject, subject + d.n_rows());
+}
+
+// ---------------------------------------------------------------- resample
+int ref_fold_assignment(void* h, int folds, uint64_t seed, int32_t* out) {
+    return guard([&] {
+        const auto f = fold_assignment(static_cast<Dataset*>(h)->data, folds, seed);
+        for (std::size_t i = 0; i < f.size(); ++i) out[i] = f[i];
+    });
+}
+
+int ref_kfold_select_gamma(void* h, const double* tmpl, int folds, const double* grid, int64_t ng,
+                           uint64_t seed, int max_cycles, double tolerance, double initial_trust,
+                           int workers, double* fold_scores, double* mean_scores,
+                           double* gamma_star, int* n_warnings) {
+    return guard([&] {
+        const auto& d = static_cast<Dataset*>(h)->data;
+        PenaltySpec pen{std::vector<double>(tmpl, tmpl + d.n_covariates())};
+        CvConfig cv;
+        cv.folds = folds;
+        cv.gamma_grid.assign(grid, grid + ng);
+        cv.seed = seed;
+        OptimizerConfig cfg;
+        cfg.max_cycles = max_cycles;
+        cfg.tolerance = tolerance;
+        cfg.initial_trust = initial_trust;
+        cfg.exec = exec_of(0, workers);
+        const CvResult r = kfold_select_gamma(d, pen, cv, cfg);
+        for (int64_t g = 0; g < ng; ++g) {
+            mean_scores[g] = r.mean_scores[static_cast<std::size_t>(g)];
+            for (int f = 0; f < folds; ++f)
+                fold_scores[g * folds + f] = r.fold_scores[static_cast<std::size_t>(g)][static_cast<std::size_t>(f)];
+        }
+        *gamma_star = r.gamma_star;
+        *n_warnings = static_cast<int>(r.warnings.size());
+    });
+}
+
 // ---------------------------------------------------------------- design
 int ref_design_build(void* dataset, void** out) {
     return guard([&] {

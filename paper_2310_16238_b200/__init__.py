@@ -22,8 +22,13 @@ from .stratcox import (  # noqa: F401
     StratcoxError,
     TrustOutcome,
     ValidationError,
+    CvResult,
+    SurvivalDataset,
     apply_trust_region,
+    build_design,
     ccd_fit,
+    fold_assignment,
+    kfold_select_gamma,
     default_gamma_grid,
     device_count,
     gamma_max,

@@ -85,6 +85,37 @@ SIGNATURES = {
     "scx_comm_destroy": (C.c_int, [_vp]),
 }
 
+class DatasetC(C.Structure):
+    """scx_dataset"""
+    _fields_ = [("n_rows", C.c_int64), ("time", C.POINTER(C.c_double)),
+                ("event", C.POINTER(C.c_uint8)), ("stratum", C.POINTER(C.c_int32)),
+                ("subject", C.POINTER(C.c_int64)), ("n_covariates", C.c_int64),
+                ("col_ptr", C.POINTER(C.c_int64)), ("row_idx", C.POINTER(C.c_int64)),
+                ("values", C.POINTER(C.c_double))]
+
+
+class CvConfigC(C.Structure):
+    """scx_cv_config"""
+    _fields_ = [("folds", C.c_int), ("gamma_grid", C.POINTER(C.c_double)),
+                ("grid_size", C.c_int64), ("seed", C.c_uint64)]
+
+
+class CvResultC(C.Structure):
+    """scx_cv_result"""
+    _fields_ = [("gamma_star", C.c_double), ("fold_scores", C.POINTER(C.c_double)),
+                ("mean_scores", C.POINTER(C.c_double)), ("n_warnings", C.c_int32)]
+
+
+SIGNATURES.update({
+    "scx_build_design": (C.c_int, [_vp, C.POINTER(DatasetC), _i64p]),
+    "scx_default_gamma_grid": (C.c_int, [C.c_double, C.c_int64, _dp]),
+    "scx_fold_assignment": (C.c_int, [C.POINTER(DatasetC), C.c_int, C.c_uint64,
+                                      C.POINTER(C.c_int32)]),
+    "scx_kfold_select_gamma": (C.c_int, [C.POINTER(DatasetC), _dp, C.POINTER(CvConfigC),
+                                         C.POINTER(FitOptions), C.POINTER(C.c_int), C.c_int,
+                                         C.POINTER(CvResultC), C.c_char_p, C.c_int]),
+})
+
 _lib = None
 
 

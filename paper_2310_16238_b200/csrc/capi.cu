@@ -451,6 +451,12 @@ __global__ void k_k3_check(const int32_t* rows, const double* vals, const double
 
 }  // namespace
 
+// Record a message on a context (read back by scx_last_error); used by the
+// drivers in cv.cu.
+void scx_note_error(scx_ctx* ctx, const char* msg) {
+    if (ctx) ctx->err = msg;
+}
+
 
 // =================================================================== C-ABI
 extern "C" {

@@ -517,3 +517,117 @@ def default_gamma_grid(gamma_max_value: float, size: int = 20) -> np.ndarray:
         t = 1.0 if size == 1 else i / (size - 1)
         out[i] = math.exp(lo + t * (hi - lo))
     return out
+
+
+# ---------------------------------------------------------------- data sets, path and CV
+@dataclass
+class SurvivalDataset:
+    """SurvivalDataset (data.hpp:31-45) in input row order, CSC columns."""
+    time: np.ndarray
+    event: np.ndarray
+    stratum: np.ndarray
+    col_ptr: np.ndarray
+    row_idx: np.ndarray
+    values: Optional[np.ndarray] = None
+    subject: Optional[np.ndarray] = None
+
+    def n_rows(self) -> int:
+        return int(self.time.shape[0])
+
+    def n_covariates(self) -> int:
+        return int(self.col_ptr.shape[0] - 1)
+
+    def _c(self):
+        keep = dict(time=np.ascontiguousarray(self.time, np.float64),
+                    event=np.ascontiguousarray(self.event, np.uint8),
+                    stratum=np.ascontiguousarray(self.stratum, np.int32),
+                    col_ptr=np.ascontiguousarray(self.col_ptr, np.int64),
+                    row_idx=np.ascontiguousarray(self.row_idx, np.int64),
+                    values=None if self.values is None else np.ascontiguousarray(self.values, np.float64),
+                    subject=None if self.subject is None else np.ascontiguousarray(self.subject, np.int64))
+        ds = _capi.DatasetC(self.n_rows(), ptr(keep["time"], C.c_double), ptr(keep["event"], C.c_uint8),
+                            ptr(keep["stratum"], C.c_int32), ptr(keep["subject"], C.c_int64),
+                            self.n_covariates(), ptr(keep["col_ptr"], C.c_int64),
+                            ptr(keep["row_idx"], C.c_int64), ptr(keep["values"], C.c_double))
+        return ds, keep
+
+
+class _BuiltDesign:
+    """Shape of a design sorted and uploaded by the library (scx_build_design)."""
+
+    def __init__(self, n, k, p):
+        self.n_rows, self.n_strata, self.n_covariates = n, k, p
+
+    @staticmethod
+    def covariate_name(j: int) -> str:
+        return f"x{j + 1}"
+
+
+def build_design(data: SurvivalDataset, device: int = 0):
+    """build_sorted_design (data.hpp:66, data.cpp:68-147) + upload: returns
+    (DeviceDesign, perm) with perm[s] = input row of sorted row s."""
+    lib = _lib()
+    h = C.c_void_p()
+    if lib.scx_create(int(device), C.byref(h)) != 0:
+        raise CudaError(f"scx_create(device={device}) failed: no usable sm_100 device")
+    ds, keep = data._c()
+    perm = np.empty(data.n_rows(), np.int64)
+    rc = lib.scx_build_design(h, C.byref(ds), ptr(perm, C.c_int64))
+    if rc != 0:
+        msg = lib.scx_last_error(h).decode()
+        lib.scx_destroy(h)
+        raise _ERR.get(rc, StratcoxError)(msg)
+    dd = DeviceDesign.__new__(DeviceDesign)
+    dd._h, dd.device, dd._state_owner = h, device, None
+    info = dd.info()
+    dd.design = _BuiltDesign(info["n_rows"], info["n_strata"], info["p"])
+    return dd, perm
+
+
+def fold_assignment(data: SurvivalDataset, folds: int, seed: int) -> np.ndarray:
+    """fold_assignment (resample.hpp:45, resample.cpp:70-91)."""
+    ds, keep = data._c()
+    out = np.empty(data.n_rows(), np.int32)
+    rc = _lib().scx_fold_assignment(C.byref(ds), int(folds), int(seed), ptr(out, C.c_int32))
+    if rc:
+        raise _ERR.get(rc, StratcoxError)(
+            "folds must be >= 2" if folds < 2 else "degenerate fold; reduce folds or reseed")
+    return out
+
+
+@dataclass
+class CvResult:
+    """CvResult (resample.hpp:21-27)."""
+    gamma_star: float
+    grid: np.ndarray
+    fold_scores: np.ndarray   # [grid index][fold]
+    mean_scores: np.ndarray   # [grid index]
+    warnings: List[str]
+
+
+def kfold_select_gamma(data: SurvivalDataset, penalty_template: PenaltySpec, folds: int,
+                       gamma_grid, seed: int = 1, config: Optional[OptimizerConfig] = None,
+                       devices: Sequence[int] = (0,)) -> CvResult:
+    """kfold_select_gamma (resample.hpp:53-54): warm-started gamma path per fold
+    on the device(s), held-out stratified partial-likelihood scoring; folds are
+    dealt round-robin over ``devices``."""
+    config = config or OptimizerConfig()
+    grid = np.ascontiguousarray(gamma_grid, np.float64)
+    tmpl = np.ascontiguousarray(penalty_template.gamma, np.float64)
+    ds, keep = data._c()
+    cv = _capi.CvConfigC(int(folds), ptr(grid, C.c_double), grid.shape[0], int(seed))
+    opt = _capi.FitOptions(int(config.max_cycles), float(config.tolerance),
+                           float(config.initial_trust))
+    fs = np.zeros((grid.shape[0], max(1, folds)), np.float64)
+    ms = np.zeros(grid.shape[0], np.float64)
+    res = _capi.CvResultC(0.0, ptr(fs, C.c_double), ptr(ms, C.c_double), 0)
+    devs = (C.c_int * len(devices))(*devices)
+    msg = C.create_string_buffer(1 << 16)
+    rc = _lib().scx_kfold_select_gamma(C.byref(ds), ptr(tmpl, C.c_double), C.byref(cv),
+                                       C.byref(opt), devs, len(devices), C.byref(res), msg,
+                                       len(msg))
+    text = msg.value.decode()
+    if rc:
+        raise _ERR.get(rc, StratcoxError)(text)
+    return CvResult(gamma_star=res.gamma_star, grid=grid.copy(), fold_scores=fs, mean_scores=ms,
+                    warnings=[w for w in text.split("\n") if w])
