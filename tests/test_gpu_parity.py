@@ -414,3 +414,34 @@ def test_chunked_fit_matches_oracle(oracle, ref):
     assert r.cycles_used == want["cycles"]
     assert np.max(np.abs(r.beta - want["beta"])) <= BETA_ATOL
     assert np.allclose(r.objective_trace, want["trace"], rtol=LL_RTOL, atol=0)
+
+
+@pytest.mark.parametrize("b0", [699.5, 699.95])
+def test_fit_step_halving_vs_oracle(oracle, ref, b0):
+    """Steps that would push eta past +-700 inside the device cycle: a column held
+    at beta = b0 on the 30 latest rows (in every risk set) overlaps the other
+    columns, so their steps need the exact halving level and some are skipped
+    after 10 halvings with a warning (optimizer.cpp:110-123); against the oracle."""
+    from oracle.oracle_py import Dataset
+    ds = ref.random_dataset(7, 3000, 2, 3, 0.4, 50)
+    rows_c = np.sort(np.argsort(-ds.time)[:30]).astype(np.int64)
+    ds2 = Dataset(ds.time, ds.event.copy(), ds.stratum,
+                  np.concatenate([ds.col_ptr, [ds.col_ptr[-1] + 30]]),
+                  np.concatenate([ds.row_idx, rows_c]), np.concatenate([ds.values * 30, np.ones(30)]))
+    ds2.event[rows_c] = 0
+    a = oracle.build_sorted_design(ds2)
+    d = oracle.design(a)
+    dd = upload(a)
+    p = a["p"]
+    b_init = np.array([0.0, 0.0, 0.0, b0])
+    want = oracle.ccd_fit(d, np.zeros(p), max_cycles=6, tol=1e-9, initial_trust=1.0,
+                          initial_beta=b_init)
+    assert want["n_warnings"] > 0  # the design does exercise the 10-halving skip
+    r = sx.ccd_fit(dd, sx.PenaltySpec(np.zeros(p)),
+                   sx.OptimizerConfig(max_cycles=6, tolerance=1e-9, initial_trust=1.0),
+                   initial_beta=b_init)
+    assert r.cycles_used == want["cycles"]
+    assert len(r.warnings) == want["n_warnings"]
+    assert np.max(np.abs(r.beta - want["beta"])) <= BETA_ATOL
+    assert np.max(np.abs(r.trust - want["trust"]) / np.maximum(1, np.abs(want["trust"]))) <= 1e-12
+    assert np.allclose(r.objective_trace, want["trace"], rtol=LL_RTOL, atol=0)
