@@ -33,7 +33,11 @@ $(OBJDIR)/cv.o: $(CSRC)/cv.cu include/stratcox_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/cv.ptxas.txt || (cat $(OBJDIR)/cv.ptxas.txt; exit 1)
 
-$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o
+$(OBJDIR)/transforms.o: $(CSRC)/transforms.cu include/stratcox_b200.h
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/transforms.ptxas.txt || (cat $(OBJDIR)/transforms.ptxas.txt; exit 1)
+
+$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o $(OBJDIR)/transforms.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
 oracle:

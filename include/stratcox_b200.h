@@ -209,6 +209,29 @@ scx_status scx_kfold_select_gamma(const scx_dataset* data, const double* penalty
                                   const int* devices, int n_devices, scx_cv_result* result,
                                   char* error_out, int error_cap);
 
+/* ---------------------------------------------------------------- lowering (transforms.hpp)
+ * Subjects with time-fixed covariates (scx_dataset over SUBJECTS; stratum is
+ * ignored) and cut points 0 = t0 < ... < tK: make_time_varying, then
+ * split_time_varying_coefficient for the covariates listed in split_covariate
+ * (split times of split s: split_times[split_ptr[s] .. split_ptr[s+1]), each a
+ * cut point), then augment_to_strata (transforms.cpp:64-223): one row per
+ * (subject, interval at risk), interval-major, stratum = interval. The result
+ * is library-owned: sizes, a scx_dataset view (feed it to scx_build_design or
+ * scx_kfold_select_gamma) and the column map (source covariate, effect window
+ * -1 = unsplit, window bounds). */
+typedef struct scx_lowered scx_lowered;
+scx_status scx_lower_time_varying(const scx_dataset* subjects, const double* cut_points,
+                                  int64_t n_cuts, const int64_t* split_covariate,
+                                  const int64_t* split_ptr, const double* split_times,
+                                  int64_t n_splits, scx_lowered** out, char* error_out,
+                                  int error_cap);
+scx_status scx_lowered_sizes(const scx_lowered* lowered, int64_t* n_rows, int64_t* n_covariates,
+                             int64_t* nnz);
+scx_status scx_lowered_dataset(const scx_lowered* lowered, scx_dataset* view);
+scx_status scx_lowered_column_map(const scx_lowered* lowered, int64_t* source, int32_t* window,
+                                  double* window_start, double* window_end);
+void scx_lowered_free(scx_lowered* lowered);
+
 /* ---------------------------------------------------------------- measurement
  * Device time of the kernels launched by the last call, for bench/roofline:
  * per-kernel-class accumulated milliseconds and launch counts since the last

@@ -111,6 +111,8 @@ class Ref:
             "ref_dataset_subject": (None, [_vp, _i64]),
             "ref_dataset_set_subject": (None, [_vp, _i64]),
             "ref_fold_assignment": (C.c_int, [_vp, C.c_int, C.c_uint64, _i32]),
+            "ref_lower_pipeline": (C.c_int, [_vp, _d, C.c_int64, _i64, _i64, _d, C.c_int64,
+                                             C.POINTER(_vp), _i64, _i32]),
             "ref_kfold_select_gamma": (C.c_int, [_vp, _d, C.c_int, _d, C.c_int64, C.c_uint64,
                                                  C.c_int, C.c_double, C.c_double, C.c_int, _d,
                                                  _d, _d, _ip]),
@@ -326,6 +328,39 @@ def _ref_resample_methods():
         finally:
             self.L.ref_dataset_free(h)
 
+    def lower_pipeline(self, ds, cuts, splits=None, subject=None):
+        """make_time_varying + lower_pipeline (transforms.cpp:64-231) of the
+        reference; returns (Dataset, subjects, map_source, map_window)."""
+        h = self.dataset_handle(ds)
+        try:
+            if subject is not None:
+                sj = np.ascontiguousarray(subject, np.int64)
+                self.L.ref_dataset_set_subject(h, _p(sj, C.c_int64))
+            splits = splits or {}
+            cov = np.array(sorted(splits), np.int64)
+            ptr = np.zeros(len(cov) + 1, np.int64)
+            times = []
+            for q, j in enumerate(cov):
+                times += list(splits[int(j)])
+                ptr[q + 1] = len(times)
+            tm = np.array(times, np.float64) if times else np.zeros(1)
+            cu = np.ascontiguousarray(cuts, np.float64)
+            out = _vp()
+            ms = np.zeros(ds.p * (len(cuts) + 1), np.int64)
+            mw = np.zeros(ds.p * (len(cuts) + 1), np.int32)
+            self._chk(self.L.ref_lower_pipeline(h, _p(cu, C.c_double), cu.shape[0],
+                                                _p(cov if len(cov) else np.zeros(1, np.int64), C.c_int64),
+                                                _p(ptr, C.c_int64), _p(tm, C.c_double), len(cov),
+                                                C.byref(out), _p(ms, C.c_int64), _p(mw, C.c_int32)))
+            low = self._dataset(out)
+            subj = np.empty(low.n, np.int64)
+            self.L.ref_dataset_subject(out, _p(subj, C.c_int64))
+            self.L.ref_dataset_free(out)
+            return low, subj, ms[:low.p], mw[:low.p]
+        finally:
+            self.L.ref_dataset_free(h)
+
+    Ref.lower_pipeline = lower_pipeline
     Ref.fold_assignment = fold_assignment
     Ref.kfold_select_gamma = kfold_select_gamma
 

@@ -30,6 +30,7 @@
 #include "stratcox/likelihood.hpp"
 #include "stratcox/optimizer.hpp"
 #include "stratcox/resample.hpp"
+#include "stratcox/transforms.hpp"
 #include "stratcox/scan.hpp"
 #include "stratcox/simulate.hpp"
 
@@ -183,6 +184,33 @@ void ref_dataset_subject(void* h, int64_t* out) {
 void ref_dataset_set_subject(void* h, const int64_t* subject) {
     auto& d = static_cast<Dataset*>(h)->data;
     d.subject.assign(subject, subject + d.n_rows());
+}
+
+// ---------------------------------------------------------------- lowering
+// make_time_varying (time-fixed columns of the subject dataset h) + lower_pipeline.
+int ref_lower_pipeline(void* h, const double* cuts, int64_t n_cuts, const int64_t* split_cov,
+                       const int64_t* split_ptr, const double* split_times, int64_t n_splits,
+                       void** out, int64_t* map_source, int32_t* map_window) {
+    return guard([&] {
+        const auto& d = static_cast<Dataset*>(h)->data;
+        std::vector<std::string> names;
+        TimeVaryingDataset tv = make_time_varying(d.time, d.event, d.subject, d.columns, names,
+                                                  std::vector<double>(cuts, cuts + n_cuts));
+        TimeVaryingSpec spec;
+        spec.cut_points.assign(cuts, cuts + n_cuts);
+        for (int64_t s = 0; s < n_splits; ++s) {
+            TimeVaryingSpec::Split sp;
+            sp.covariate = static_cast<std::size_t>(split_cov[s]);
+            sp.times.assign(split_times + split_ptr[s], split_times + split_ptr[s + 1]);
+            spec.splits.push_back(sp);
+        }
+        LoweredDataset low = lower_pipeline(tv, spec);
+        for (std::size_t c = 0; c < low.column_map.size(); ++c) {
+            map_source[c] = static_cast<int64_t>(low.column_map[c].source);
+            map_window[c] = low.column_map[c].window;
+        }
+        *out = new Dataset{std::move(low.data), {}};
+    });
 }
 
 // ---------------------------------------------------------------- resample

@@ -29,6 +29,7 @@ from .stratcox import (  # noqa: F401
     ccd_fit,
     fold_assignment,
     kfold_select_gamma,
+    lower_time_varying,
     default_gamma_grid,
     device_count,
     gamma_max,

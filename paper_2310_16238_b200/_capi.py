@@ -111,6 +111,12 @@ SIGNATURES.update({
     "scx_default_gamma_grid": (C.c_int, [C.c_double, C.c_int64, _dp]),
     "scx_fold_assignment": (C.c_int, [C.POINTER(DatasetC), C.c_int, C.c_uint64,
                                       C.POINTER(C.c_int32)]),
+    "scx_lower_time_varying": (C.c_int, [C.POINTER(DatasetC), _dp, C.c_int64, _i64p, _i64p, _dp,
+                                         C.c_int64, C.POINTER(_vp), C.c_char_p, C.c_int]),
+    "scx_lowered_sizes": (C.c_int, [_vp, _i64p, _i64p, _i64p]),
+    "scx_lowered_dataset": (C.c_int, [_vp, C.POINTER(DatasetC)]),
+    "scx_lowered_column_map": (C.c_int, [_vp, _i64p, C.POINTER(C.c_int32), _dp, _dp]),
+    "scx_lowered_free": (None, [_vp]),
     "scx_kfold_select_gamma": (C.c_int, [C.POINTER(DatasetC), _dp, C.POINTER(CvConfigC),
                                          C.POINTER(FitOptions), C.POINTER(C.c_int), C.c_int,
                                          C.POINTER(CvResultC), C.c_char_p, C.c_int]),

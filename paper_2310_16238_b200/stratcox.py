@@ -631,3 +631,59 @@ def kfold_select_gamma(data: SurvivalDataset, penalty_template: PenaltySpec, fol
         raise _ERR.get(rc, StratcoxError)(text)
     return CvResult(gamma_star=res.gamma_star, grid=grid.copy(), fold_scores=fs, mean_scores=ms,
                     warnings=[w for w in text.split("\n") if w])
+
+
+# ---------------------------------------------------------------- lowering (transforms.hpp)
+@dataclass
+class ColumnMapEntry:
+    """ColumnMapEntry (transforms.hpp:52-60): window -1 = never split."""
+    column: int
+    source: int
+    window: int
+    window_start: float
+    window_end: float
+
+
+def lower_time_varying(subjects: SurvivalDataset, cut_points, splits=None):
+    """make_time_varying (time-fixed covariates) + split_time_varying_coefficient +
+    augment_to_strata (transforms.hpp:85-104, lower_pipeline): one row per
+    (subject, interval at risk), interval-major, stratum = interval. ``splits``
+    maps a covariate index to its effect-window boundaries (cut points).
+    Returns (SurvivalDataset, [ColumnMapEntry])."""
+    lib = _lib()
+    splits = splits or {}
+    cov = np.array(sorted(splits), np.int64)
+    sptr = np.zeros(len(cov) + 1, np.int64)
+    times = []
+    for q, j in enumerate(cov):
+        times += [float(t) for t in splits[int(j)]]
+        sptr[q + 1] = len(times)
+    tm = np.array(times, np.float64)
+    cuts = np.ascontiguousarray(cut_points, np.float64)
+    ds, keep = subjects._c()
+    h = C.c_void_p()
+    msg = C.create_string_buffer(4096)
+    rc = lib.scx_lower_time_varying(C.byref(ds), ptr(cuts, C.c_double), cuts.shape[0],
+                                    ptr(cov, C.c_int64), ptr(sptr, C.c_int64), ptr(tm, C.c_double),
+                                    len(cov), C.byref(h), msg, len(msg))
+    if rc:
+        raise _ERR.get(rc, StratcoxError)(msg.value.decode())
+    try:
+        n = C.c_int64(); p = C.c_int64(); z = C.c_int64()
+        lib.scx_lowered_sizes(h, C.byref(n), C.byref(p), C.byref(z))
+        n, p, z = n.value, p.value, z.value
+        v = _capi.DatasetC()
+        lib.scx_lowered_dataset(h, C.byref(v))
+        arr = lambda pt, cnt, dt: np.ctypeslib.as_array(pt, shape=(max(cnt, 1),))[:cnt].astype(dt, copy=True)
+        out = SurvivalDataset(time=arr(v.time, n, np.float64), event=arr(v.event, n, np.uint8),
+                              stratum=arr(v.stratum, n, np.int32), col_ptr=arr(v.col_ptr, p + 1, np.int64),
+                              row_idx=arr(v.row_idx, z, np.int64), values=arr(v.values, z, np.float64),
+                              subject=arr(v.subject, n, np.int64))
+        src = np.empty(p, np.int64); win = np.empty(p, np.int32)
+        ws = np.empty(p); we = np.empty(p)
+        lib.scx_lowered_column_map(h, ptr(src, C.c_int64), win.ctypes.data_as(C.POINTER(C.c_int32)),
+                                   ptr(ws, C.c_double), ptr(we, C.c_double))
+        cmap = [ColumnMapEntry(c, int(src[c]), int(win[c]), float(ws[c]), float(we[c])) for c in range(p)]
+        return out, cmap
+    finally:
+        lib.scx_lowered_free(h)
