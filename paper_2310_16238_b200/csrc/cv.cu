@@ -16,6 +16,7 @@
 // folds are dealt round-robin over the given devices, one host thread per
 // device (the reference runs folds in an OpenMP loop, resample.cpp:121).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -125,16 +126,49 @@ struct Sorted {
     int32_t k = 0;
 };
 
+// Worker threads for the host preparation (design build, CV folds' subsets).
+int host_threads() {
+    const unsigned h = std::thread::hardware_concurrency();
+    return (int)std::max(1u, std::min(h, 32u));
+}
+
+template <class F>
+void parallel_for(int64_t count, F&& body) {
+    const int nt = (int)std::min<int64_t>(host_threads(), std::max<int64_t>(count, 1));
+    if (nt <= 1) {
+        for (int64_t i = 0; i < count; ++i) body(i);
+        return;
+    }
+    std::atomic<int64_t> next{0};
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&] {
+            for (int64_t i; (i = next.fetch_add(1)) < count;) body(i);
+        });
+    for (auto& th : pool) th.join();
+}
+
+// The reference's std::stable_sort by (stratum asc, time desc) is done as a
+// stable counting sort by stratum followed by a stable sort by time desc
+// inside each stratum (in parallel over strata): the same permutation.
 Sorted build_sorted(const Data& data) {
     validate(data);
     const int64_t n = data.n();
     if (n == 0) throw ScxError(SCX_ERR_VALIDATION, "dataset has no rows");
     Sorted s;
+    const int32_t kc = data.n_strata();
+    std::vector<int64_t> start(kc + 2, 0);
+    for (int64_t i = 0; i < n; ++i) ++start[data.stratum[i] + 1];
+    for (int32_t k = 1; k <= kc + 1; ++k) start[k] += start[k - 1];
     s.perm.resize(n);
-    std::iota(s.perm.begin(), s.perm.end(), int64_t{0});
-    std::stable_sort(s.perm.begin(), s.perm.end(), [&](int64_t a, int64_t b) {
-        if (data.stratum[a] != data.stratum[b]) return data.stratum[a] < data.stratum[b];
-        return data.time[a] > data.time[b];
+    {
+        std::vector<int64_t> fill(start.begin(), start.end());
+        for (int64_t i = 0; i < n; ++i) s.perm[fill[data.stratum[i]]++] = i;
+    }
+    parallel_for(kc, [&](int64_t q) {
+        const int32_t k = (int32_t)q + 1;
+        std::stable_sort(s.perm.begin() + start[k], s.perm.begin() + start[k + 1],
+                         [&](int64_t a, int64_t b) { return data.time[a] > data.time[b]; });
     });
     std::vector<int64_t> inverse(n);
     for (int64_t i = 0; i < n; ++i) inverse[s.perm[i]] = i;
@@ -150,9 +184,9 @@ Sorted build_sorted(const Data& data) {
     s.col_ptr = data.col_ptr;
     s.rows.resize(data.rows.size());
     s.values.resize(data.values.size());
-    std::vector<std::pair<int64_t, double>> buf;
-    for (int64_t j = 0; j < p; ++j) {
-        buf.clear();
+    parallel_for(p, [&](int64_t j) {
+        std::vector<std::pair<int64_t, double>> buf;
+        buf.reserve(data.col_ptr[j + 1] - data.col_ptr[j]);
         for (int64_t t = data.col_ptr[j]; t < data.col_ptr[j + 1]; ++t)
             buf.emplace_back(inverse[data.rows[t]], data.values[t]);
         std::sort(buf.begin(), buf.end(),
@@ -161,7 +195,7 @@ Sorted build_sorted(const Data& data) {
             s.rows[data.col_ptr[j] + t] = buf[t].first;
             s.values[data.col_ptr[j] + t] = buf[t].second;
         }
-    }
+    });
     s.offsets.push_back(0);
     for (int64_t i = 1; i < n; ++i)
         if (sstr[i] != sstr[i - 1]) s.offsets.push_back(i);

@@ -13,12 +13,14 @@
 // instead of materialising the per-interval schedules; the output arrays are
 // identical to the reference's lower_pipeline.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/stratcox_b200.h"
@@ -140,32 +142,46 @@ scx_status scx_lower_time_varying(const scx_dataset* subj, const double* cut_poi
             edges.push_back(cuts.back());
             for (size_t w = 0; w + 1 < edges.size(); ++w) cols.push_back({j, (int)w, edges[w], edges[w + 1]});
         }
-        // augment_to_strata (:177-223): interval-major rows, subjects in input order
-        std::vector<std::vector<std::pair<int64_t, double>>> acc(cols.size());
-        std::vector<int64_t> rank(n);
+        // augment_to_strata (:177-223): interval-major rows, subjects in input
+        // order; rank[k-1][i] = augmented row of subject i in interval k (-1: not at risk)
+        std::vector<std::vector<int64_t>> rank(k_count, std::vector<int64_t>(n, -1));
         for (int k = 1; k <= k_count; ++k) {
             const int64_t offset = (int64_t)L->time.size();
             int64_t emitted = 0;
             for (int64_t i = 0; i < n; ++i) {
-                rank[i] = -1;
                 if (!at_risk(subj->time[i], subj->event[i], k, cuts)) continue;
-                rank[i] = offset + emitted++;
+                rank[k - 1][i] = offset + emitted++;
                 L->time.push_back(std::min(subj->time[i], cuts[k]));
                 L->event.push_back(subj->event[i] && event_interval(subj->time[i], cuts) == k ? 1 : 0);
                 L->stratum.push_back(k);
                 L->subject.push_back(subject[i]);
             }
-            for (size_t c = 0; c < cols.size(); ++c) {
-                const OutCol& oc = cols[c];
-                // window w's column carries interval k iff t_{k-1} in [start, end)
-                if (oc.window >= 0 && !(cuts[k - 1] >= oc.start && cuts[k - 1] < oc.end)) continue;
-                const int64_t j = oc.src;
-                for (int64_t t = subj->col_ptr[j]; t < subj->col_ptr[j + 1]; ++t) {
-                    const int64_t i = subj->row_idx[t];
-                    const double v = subj->values ? subj->values[t] : 1.0;
-                    if (rank[i] >= 0 && v != 0.0) acc[c].emplace_back(rank[i], v);
-                }
-            }
+        }
+        // columns are independent: one worker per column, intervals in order
+        std::vector<std::vector<std::pair<int64_t, double>>> acc(cols.size());
+        {
+            std::atomic<size_t> next{0};
+            const unsigned nt = std::max(1u, std::min(std::thread::hardware_concurrency(), 32u));
+            std::vector<std::thread> pool;
+            for (unsigned w = 0; w < nt; ++w)
+                pool.emplace_back([&] {
+                    for (size_t c; (c = next.fetch_add(1)) < cols.size();) {
+                        const OutCol& oc = cols[c];
+                        const int64_t j = oc.src;
+                        for (int k = 1; k <= k_count; ++k) {
+                            // window w's column carries interval k iff t_{k-1} in [start, end)
+                            if (oc.window >= 0 && !(cuts[k - 1] >= oc.start && cuts[k - 1] < oc.end))
+                                continue;
+                            const std::vector<int64_t>& rk = rank[k - 1];
+                            for (int64_t t = subj->col_ptr[j]; t < subj->col_ptr[j + 1]; ++t) {
+                                const int64_t i = subj->row_idx[t];
+                                const double v = subj->values ? subj->values[t] : 1.0;
+                                if (rk[i] >= 0 && v != 0.0) acc[c].emplace_back(rk[i], v);
+                            }
+                        }
+                    }
+                });
+            for (auto& th : pool) th.join();
         }
         L->col_ptr.push_back(0);
         for (size_t c = 0; c < cols.size(); ++c) {
