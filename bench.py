@@ -566,7 +566,12 @@ def main():
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (device generator restating simulate.cpp's model; seed 11)",
-            "config": {"workload": WORKLOAD, "n_rows": args.n, "p": args.p, "strata": args.k,
+            "config": {"workload": WORKLOAD if (args.n, args.p, args.k, args.density) ==
+                       (10_000_000, 10_000, 1000, 0.01) else
+                       (f"C5 shape on one GPU: stratified Cox L1 CCD fit, N={args.n:.0e} rows, "
+                        f"p={args.p} sparse indicator covariates ({args.density:g} density), "
+                        f"K={args.k} strata, gamma=0.05*gamma_max, beta0=0, tol=1e-6"),
+                       "n_rows": args.n, "p": args.p, "strata": args.k,
                        "density": args.density, "nnz": syn.nnz, "gamma": gamma,
                        "gamma_max": gmax, "fit_cycles": cycles, "evals_per_step": evals,
                        "code_bytes": info["code_bytes"],
