@@ -1157,9 +1157,22 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
             // the whole cycle on the device: one cooperative launch per run of
             // same-kind columns (one launch for an all-indicator design)
             for (const auto& run : ctx->runs) {
-                tmark(ctx, 0);
-                KL(1, launch_cycle(d, ctx->cols_d + run[0], run[1], run[2] != 0, s));
-                tend(ctx);
+                int32_t done = 0;
+                while (done < run[1]) {
+                    const int izero = 0;
+                    CK(cudaMemcpyAsync(&d.ctl->resume, &izero, sizeof izero, cudaMemcpyHostToDevice, s));
+                    tmark(ctx, 0);
+                    KL(1, launch_cycle(d, ctx->cols_d + run[0] + done, run[1] - done, run[2] != 0, s));
+                    tend(ctx);
+                    if (scx_status st = read_ctl(ctx)) return st;
+                    if (ctx->ctl_h->err_kind) return map_error(ctx, -1);
+                    const int32_t r = ctx->ctl_h->resume;
+                    if (r <= 0) break;
+                    // 256 accepted updates: refresh eta/D from beta, then resume
+                    done += r;
+                    KL(2, launch_refresh(d, s));
+                    if (scx_status st = check_device_error(ctx)) return st;
+                }
             }
         } else {
             for (int64_t j = 0; j < p; ++j) {

@@ -98,6 +98,8 @@ struct DevCtl {
     long long n_eval;       // gradient/Hessian evaluations
     double part[4];         // multi-GPU: (local lin, ratio sum, variance sum, 0)
     long long warn_coord[64];
+    int resume;     // cycle kernel: coordinates done before it stopped for a refresh (0: ran to the end)
+    int pad3;
 };
 
 struct Pref1 {
