@@ -461,13 +461,39 @@ def main():
             evals.append(r.n_evaluations)
             cycles.append(r.cycles_used)
     launches = lib.scx_launch_count(h) - launches0
+    path_stats = dd.fit_path_stats()
+    log(f"[bench] fit path stats {path_stats}")
     ms_step = float(np.mean(times))
     value = float(np.mean(evals)) / (ms_step / 1e3)
     beta_fit = r.beta.copy()
 
-    # ---- roofline: K1 alone, L2 flushed before each launch
+    # ---- roofline. The fit on the chunked layout runs the risk-suffix cycle:
+    # its O(N) work is the fused risk scan (S0 -> w/S0, w/S0^2 -> within-stratum
+    # prefixes U, V written per row), once per cycle launch and once per
+    # applied step; a coordinate itself is O(nnz_j) gathers. The dominant
+    # kernel's roofline is that scan, timed alone (scx_risk_prefix, one launch
+    # = every chunk once), L2 flushed before each launch. Algorithmic bytes
+    # per row: D 8 + event code + (U, V) 16 written.
+    import ctypes as C
+    tot = C.c_double()
+    nl = C.c_int64()
     lib.scx_timing_enable(h, 1)
     st = sx.make_state(dd, beta_fit)
+    rs_on = dd.set_fit_path(0)
+    row_bytes_rs = 8 + info["code_bytes"] + 16
+    rs = None
+    if rs_on:
+        lib.scx_timing_reset(h)
+        for _ in range(24):
+            flush_l2(l2buf)
+            torch.cuda.synchronize(dev)
+            assert lib.scx_risk_prefix(h) == 0
+        lib.scx_timing_get(h, 3, C.byref(tot), C.byref(nl))
+        rs_ms = tot.value / max(1, nl.value)
+        rs_bytes = design.n_rows * row_bytes_rs
+        rs = {"ms": rs_ms, "bytes": rs_bytes, "gbs": rs_bytes / (rs_ms * 1e-3) / 1e9}
+    # the per-coordinate fused scan+reduce (K1: gradient_hessian, and the fit's
+    # exact path), L2 flushed before each launch
     nz_cols = [j for j in range(p) if design.col_ptr[j + 1] > design.col_ptr[j]]
     sample = nz_cols[:: max(1, len(nz_cols) // 48)][:48]
     lib.scx_timing_reset(h)
@@ -475,34 +501,53 @@ def main():
         flush_l2(l2buf)
         torch.cuda.synchronize(dev)
         sx.gradient_hessian(dd, st, j)
-    import ctypes as C
-    tot = C.c_double()
-    nl = C.c_int64()
     lib.scx_timing_get(h, 0, C.byref(tot), C.byref(nl))
     k1_ms = tot.value / max(1, nl.value)
     nnz_mean = float(np.mean([design.col_ptr[j + 1] - design.col_ptr[j] for j in sample]))
-    row_bytes = 8 + info["code_bytes"]
-    alg_bytes = design.n_rows * row_bytes + 4 * nnz_mean
-    achieved = alg_bytes / (k1_ms * 1e-3) / 1e9
-    # Inside the fit: one cooperative launch per CCD cycle runs every
-    # coordinate (fused scan+reduce, on-device rule, eta/D update); per
-    # coordinate = cycle-kernel time / coordinates with nnz > 0 (warm L2).
-    n_coords = sum(1 for j in range(p) if design.col_ptr[j + 1] > design.col_ptr[j])
+    k1_bytes = design.n_rows * (8 + info["code_bytes"]) + 4 * nnz_mean
+    # inside the fit (warm): time of the cycle kernels over one full CCD cycle
+    n_coords = len(nz_cols)
     lib.scx_timing_reset(h)
     sx.ccd_fit(dd, pen, sx.OptimizerConfig(max_cycles=1))
+    lib.scx_timing_get(h, 3, C.byref(tot), C.byref(nl))
+    rs_cycle_ms, rs_launches = tot.value, nl.value
     lib.scx_timing_get(h, 0, C.byref(tot), C.byref(nl))
-    cycle_ms = tot.value / max(1, nl.value)
-    coord_ms = tot.value / max(1, n_coords)
+    fs_cycle_ms, fs_launches = tot.value, nl.value
     lib.scx_timing_enable(h, 0)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_k1_summary.json")
-    if os.path.exists(prof):
+    in_fit = {"cycle1_risk_suffix_ms": rs_cycle_ms, "cycle1_risk_suffix_launches": rs_launches,
+              "cycle1_fused_scan_ms": fs_cycle_ms, "cycle1_fused_scan_launches": fs_launches,
+              "cycle1_ms_per_coordinate": (rs_cycle_ms + fs_cycle_ms) / max(1, n_coords)}
+
+    def ncu_traffic(name, rows):
+        f = os.path.join(ROOT, "profiles", name)
         try:
-            pj = json.load(open(prof))
-            if pj.get("n_rows") == design.n_rows:
-                traffic = pj.get("dram_bytes_per_launch")
+            pj = json.load(open(f))
+            return pj.get("dram_bytes_per_launch") if pj.get("n_rows") == rows else None
         except Exception:
-            traffic = None
+            return None
+
+    if rs is not None:
+        roof = {"bound": "hbm", "achieved": rs["gbs"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": rs["gbs"] / hbm_peak,
+                "traffic": ncu_traffic("ncu_rs_prefix_summary.json", design.n_rows),
+                "kernel": "k_rs_cycle risk prefix (fused segmented scan of D -> w/S0, w/S0^2 "
+                          "-> within-stratum prefixes)",
+                "algorithmic_bytes_per_launch": rs["bytes"],
+                "algorithmic_bytes_per_row": row_bytes_rs,
+                "avg_launch_ms": rs["ms"], "peak_source": peak_src}
+    else:
+        roof = {"bound": "hbm", "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                "unit": "GB/s", "frac": k1_bytes / (k1_ms * 1e-3) / 1e9 / hbm_peak,
+                "traffic": ncu_traffic("ncu_k1_summary.json", design.n_rows),
+                "kernel": "k1_grad_hess (fused segmented scan + g'/g'' reduce)",
+                "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_ms,
+                "peak_source": peak_src}
+    roof["in_fit"] = in_fit
+    roof["k1_fused_scan_per_coordinate"] = {
+        "avg_launch_ms": k1_ms, "algorithmic_bytes_per_launch": k1_bytes,
+        "achieved_gbs": k1_bytes / (k1_ms * 1e-3) / 1e9,
+        "frac": k1_bytes / (k1_ms * 1e-3) / 1e9 / hbm_peak,
+        "traffic": ncu_traffic("ncu_k1_summary.json", design.n_rows)}
 
     # ---- e2e through the public API from pinned host buffers
     e2e_times = []
@@ -576,18 +621,13 @@ def main():
                        "gamma_max": gmax, "fit_cycles": cycles, "evals_per_step": evals,
                        "code_bytes": info["code_bytes"],
                        "l2_flush": "256 MiB write before every timed step and before every "
-                                   "roofline K1 launch",
+                                   "roofline launch",
                        "parallelism": f"rows sharded at stratum boundaries x{world}"
                        if world > 1 else "single GPU"},
             "fit_wall_s": ms_step / 1e3,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "k1_grad_hess (fused segmented scan + g'/g'' reduce)",
-                         "algorithmic_bytes_per_launch": alg_bytes,
-                         "avg_launch_ms": k1_ms, "peak_source": peak_src,
-                         "in_fit_cycle_kernel_ms": cycle_ms,
-                         "in_fit_ms_per_coordinate": coord_ms,
-                         "in_fit_effective_gbs": alg_bytes / (coord_ms * 1e-3) / 1e9},
+            "roofline": roof,
+            "fit_path": "risk-suffix cycle" if rs_on else "fused-scan cycle",
+            "fit_path_stats": path_stats,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),

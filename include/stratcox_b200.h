@@ -99,6 +99,24 @@ scx_status scx_update_xbeta(scx_ctx* ctx, int64_t j, double delta);
 /* ---------------------------------------------------------------- likelihood */
 /* gradient_hessian (likelihood.hpp:75-77, likelihood.cpp:129-189). */
 scx_status scx_gradient_hessian(scx_ctx* ctx, int64_t j, double* gradient, double* hessian);
+/* The same (g', g'') by the risk-suffix formulation the fit uses on the chunked
+ * layout (no reference counterpart; replaces likelihood.cpp:129-189 inside
+ * run_ccd, optimizer.cpp:104): one fused scan of the state gives per row the
+ * within-stratum prefixes of w/S0 and w/S0^2, then column j costs O(nnz_j)
+ * gathers. Agrees with scx_gradient_hessian within rounding. Needs the
+ * chunked layout (many small strata); else SCX_ERR_VALIDATION. */
+scx_status scx_gradient_hessian_rs(scx_ctx* ctx, int64_t j, double* gradient, double* hessian);
+/* The risk-suffix fused scan alone over the current state (timing kind 3). */
+scx_status scx_risk_prefix(scx_ctx* ctx);
+/* CCD cycle implementation: 0 = automatic (risk-suffix cycle on the chunked
+ * layout while max|eta| <= 300, the per-coordinate fused-scan cycle otherwise
+ * and for coordinates whose g'' cancels), 1 = fused-scan cycle only.
+ * *risk_suffix (may be NULL) receives whether the risk-suffix cycle can run. */
+scx_status scx_set_fit_path(scx_ctx* ctx, int path, int* risk_suffix);
+/* Path counters of the last scx_ccd_fit: out[0] risk-suffix cycle launches,
+ * out[1] coordinates handed to the exact fused scan (rounding bound not
+ * certified), out[2] hand-offs on the |eta| bound, out[3] fused-scan cycle launches. */
+scx_status scx_fit_path_stats(const scx_ctx* ctx, int64_t out[4]);
 /* log_partial_likelihood (likelihood.hpp:60-65, likelihood.cpp:93-121). */
 scx_status scx_log_partial_likelihood(scx_ctx* ctx, double* loglik);
 /* naive_gradient_hessian / naive_log_partial_likelihood (likelihood.hpp:80-82,
@@ -238,7 +256,8 @@ void scx_lowered_free(scx_lowered* lowered);
  * scx_timing_reset. Enabled by scx_timing_enable(ctx, 1) (adds events). */
 scx_status scx_timing_enable(scx_ctx* ctx, int on);
 scx_status scx_timing_reset(scx_ctx* ctx);
-/* kind: 0 = fused scan+reduce (K1), 1 = update (K3), 2 = log-likelihood (K2) */
+/* kind: 0 = fused scan+reduce (K1), 1 = update (K3), 2 = log-likelihood (K2),
+ * 3 = risk-suffix cycle / risk prefix */
 scx_status scx_timing_get(scx_ctx* ctx, int kind, double* total_ms, int64_t* launches);
 
 /* Fused scan+reduce decomposition: 0 = automatic (stratum-aligned chunk per

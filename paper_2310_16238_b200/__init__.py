@@ -41,6 +41,7 @@ from .stratcox import (  # noqa: F401
     naive_log_partial_likelihood,
     newton_step,
     refresh_xbeta,
+    risk_suffix_gradient_hessian,
     segmented_inclusive_scan,
     state_from_arrays,
     update_xbeta,

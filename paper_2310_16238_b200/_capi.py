@@ -62,6 +62,10 @@ SIGNATURES = {
     "scx_refresh_xbeta": (C.c_int, [_vp]),
     "scx_update_xbeta": (C.c_int, [_vp, C.c_int64, C.c_double]),
     "scx_gradient_hessian": (C.c_int, [_vp, C.c_int64, _dp, _dp]),
+    "scx_gradient_hessian_rs": (C.c_int, [_vp, C.c_int64, _dp, _dp]),
+    "scx_risk_prefix": (C.c_int, [_vp]),
+    "scx_set_fit_path": (C.c_int, [_vp, C.c_int, _ip]),
+    "scx_fit_path_stats": (C.c_int, [_vp, _i64p]),
     "scx_log_partial_likelihood": (C.c_int, [_vp, _dp]),
     "scx_naive_gradient_hessian": (C.c_int, [_vp, C.c_int64, _dp, _dp]),
     "scx_naive_log_partial_likelihood": (C.c_int, [_vp, _dp]),

@@ -91,8 +91,8 @@ cudaError_t dmalloc(T** p, size_t count) {
 
 struct Timer {
     bool on = false;
-    double ms[3] = {0, 0, 0};
-    int64_t launches[3] = {0, 0, 0};
+    double ms[4] = {0, 0, 0, 0};
+    int64_t launches[4] = {0, 0, 0, 0};
     std::vector<cudaEvent_t> ev;
     std::vector<int> kinds;
     size_t used = 0;
@@ -128,6 +128,10 @@ struct scx_ctx {
     ColArgs* cols_d = nullptr;
     std::vector<std::array<int32_t, 3>> runs;
     bool per_coordinate_fit = false;  // SCX_FIT_PER_COORD=1: one K1 + K3 launch per coordinate
+    int fit_path = 0;                 // 0 auto (risk-suffix cycle when eligible), 1 fused-scan cycle
+    ColArgs* col1_d = nullptr;        // one column's ColArgs (risk-suffix evaluation)
+    int64_t rs_stats[4] = {0, 0, 0, 0};  // last fit: risk-suffix launches, exact hand-offs,
+                                         // bound hand-offs, fused-scan cycle launches
     // multi-GPU
     void* comm = nullptr;
     int nranks = 1, rank = 0;
@@ -166,13 +170,14 @@ void free_design(scx_ctx* ctx) {
                     d.trust,  d.status,     d.slots,       d.partial,   ctx->xdense,
                     ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
                     ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d, d.lasth1,
-                    d.chunk_rows, ctx->cols_d};
+                    d.chunk_rows, ctx->cols_d, d.rs_u, d.rs_R, d.rs_Q, d.chunk_k, ctx->col1_d};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     const DevCtl* keep_ctl = d.ctl;
     d = DesignDev{};
     d.ctl = const_cast<DevCtl*>(keep_ctl);
     ctx->xdense = nullptr;
+    ctx->col1_d = nullptr;
     ctx->col_beg_d = nullptr;
     ctx->val_off_d = nullptr;
     ctx->offsets_d = nullptr;
@@ -686,11 +691,31 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         }
         d.chunk_rows = nullptr;
         d.nchunks = 0;
+        d.rs_ok = 0;
         if (ok) {
             CK(dmalloc(&d.chunk_rows, ch.size()));
             CK(cudaMemcpyAsync(d.chunk_rows, ch.data(), ch.size() * sizeof(int32_t),
                                cudaMemcpyHostToDevice, s));
             d.nchunks = (int32_t)G;
+            // first stratum of each chunk (chunks start at heads) for the
+            // risk-suffix cycle, which stages a chunk's strata in shared memory
+            std::vector<int32_t> ck(ch.size());
+            int32_t q = 0;
+            int32_t most = 0;
+            for (size_t c = 0; c < ch.size(); ++c) {
+                while (q < k && offsets[q] < ch[c]) ++q;
+                ck[c] = q;
+                if (c > 0) most = std::max(most, ck[c] - ck[c - 1]);
+            }
+            if (most <= kRsMaxStrata) {
+                CK(dmalloc(&d.chunk_k, ck.size()));
+                CK(cudaMemcpyAsync(d.chunk_k, ck.data(), ck.size() * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, s));
+                CK(dmalloc(&d.rs_u, d.npad));
+                CK(dmalloc(&d.rs_R, d.npad));
+                CK(dmalloc(&d.rs_Q, d.npad));
+                d.rs_ok = 1;
+            }
         }
     }
     CK(dmalloc(&d.status, d.ntiles));
@@ -710,7 +735,9 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     d.val_off = ctx->val_off_d;
     d.offsets = ctx->offsets_d;
     if (!make_tmap(&d.tmap_D, d.D, d.npad) || !make_tmap(&d.tmap_eta, d.eta, d.npad) ||
-        !make_tmap(&d.tmap_D1, d.D, d.npad, kK1TileRows))
+        !make_tmap(&d.tmap_D1, d.D, d.npad, kK1TileRows) ||
+        (d.rs_ok && (!make_tmap(&d.tmap_u, d.rs_u, d.npad) || !make_tmap(&d.tmap_R, d.rs_R, d.npad) ||
+                     !make_tmap(&d.tmap_Q, d.rs_Q, d.npad))))
         return fail(ctx, SCX_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 
     // co-resident block count for the cooperative kernels
@@ -878,6 +905,54 @@ scx_status scx_gradient_hessian(scx_ctx* ctx, int64_t j, double* g, double* h) {
     if (scx_status s = check_device_error(ctx, (int)j)) return s;
     *g = ctx->ctl_h->g;
     *h = ctx->ctl_h->h;
+    return SCX_OK;
+}
+
+scx_status scx_gradient_hessian_rs(scx_ctx* ctx, int64_t j, double* g, double* h) {
+    if (scx_status s = need_design(ctx)) return s;
+    if (j < 0 || j >= ctx->d.p) return fail(ctx, SCX_ERR_VALIDATION, "covariate index out of range");
+    if (!ctx->d.rs_ok)
+        return fail(ctx, SCX_ERR_VALIDATION, "risk-suffix evaluation needs the chunked layout");
+    cudaSetDevice(ctx->device);
+    if (ctx->cols[j].nnz == 0) {  // no entries: (0, 0) as the fused scan gives
+        *g = 0.0;
+        *h = 0.0;
+        return SCX_OK;
+    }
+    if (!ctx->col1_d) CK(dmalloc(&ctx->col1_d, 1));
+    CK(cudaMemcpyAsync(ctx->col1_d, &ctx->cols[j], sizeof(ColArgs), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    tmark(ctx, 3);
+    KL(1, launch_rs_cycle(ctx->d, ctx->col1_d, 1, 1, ctx->stream));
+    tend(ctx);
+    tcollect(ctx);
+    if (scx_status s = check_device_error(ctx, (int)j)) return s;
+    *g = ctx->ctl_h->g;
+    *h = ctx->ctl_h->h;
+    return SCX_OK;
+}
+
+scx_status scx_risk_prefix(scx_ctx* ctx) {
+    if (scx_status s = need_design(ctx)) return s;
+    if (!ctx->d.rs_ok)
+        return fail(ctx, SCX_ERR_VALIDATION, "risk-suffix evaluation needs the chunked layout");
+    cudaSetDevice(ctx->device);
+    tmark(ctx, 3);
+    KL(1, launch_rs_cycle(ctx->d, ctx->cols_d, 0, 2, ctx->stream));
+    tend(ctx);
+    return SCX_OK;
+}
+
+scx_status scx_fit_path_stats(const scx_ctx* ctx, int64_t out[4]) {
+    if (!ctx || !out) return SCX_ERR_VALIDATION;
+    for (int q = 0; q < 4; ++q) out[q] = ctx->rs_stats[q];
+    return SCX_OK;
+}
+
+scx_status scx_set_fit_path(scx_ctx* ctx, int path, int* risk_suffix) {
+    if (!ctx || path < 0 || path > 1) return SCX_ERR_VALIDATION;
+    ctx->fit_path = path;
+    if (risk_suffix) *risk_suffix = (path == 0 && ctx->d.rs_ok && ctx->d.k1_mode != 1) ? 1 : 0;
     return SCX_OK;
 }
 
@@ -1070,6 +1145,36 @@ static scx_status run_cycle_tail(scx_ctx* ctx, bool end_of_cycle, double* ll, do
     return SCX_OK;
 }
 
+// Fused-scan cycle kernel over cols[0..n). *resumed = coordinates done before a
+// stop for the 256-update refresh (which is run here), 0 when it ran to the end;
+// with resumed == nullptr the refresh, if due, is run and nothing is reported.
+static scx_status fused_cycle(scx_ctx* ctx, const ColArgs* cols, int32_t n, bool indicator,
+                              int32_t* resumed) {
+    DesignDev& d = ctx->d;
+    cudaStream_t s = ctx->stream;
+    const int izero = 0;
+    CK(cudaMemcpyAsync(&d.ctl->resume, &izero, sizeof izero, cudaMemcpyHostToDevice, s));
+    ctx->rs_stats[3] += 1;
+    tmark(ctx, 0);
+    KL(1, launch_cycle(d, cols, n, indicator, s));
+    tend(ctx);
+    if (scx_status st = read_ctl(ctx)) return st;
+    if (ctx->ctl_h->err_kind) return map_error(ctx, -1);
+    const int32_t r = ctx->ctl_h->resume;
+    if (resumed) *resumed = r;
+    if (r > 0) {
+        // 256 accepted updates: refresh eta/D from beta, then resume
+        KL(2, launch_refresh(d, s));
+        if (scx_status st = check_device_error(ctx)) return st;
+    }
+    return SCX_OK;
+}
+
+static bool rs_usable(const scx_ctx* ctx) {
+    return ctx->fit_path == 0 && ctx->d.rs_ok && ctx->d.k1_mode != 1 &&
+           ctx->ctl_h->mbound <= kRsEtaBound;
+}
+
 static scx_status run_coordinate(scx_ctx* ctx, const ColArgs& col) {
     DesignDev& d = ctx->d;
     cudaStream_t s = ctx->stream;
@@ -1124,6 +1229,7 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
 
     std::vector<double> beta0(p, 0.0);
     if (initial_beta) std::copy(initial_beta, initial_beta + p, beta0.begin());
+    for (auto& v : ctx->rs_stats) v = 0;
     if (p > 0) {
         CK(cudaMemcpyAsync(d.gamma, gamma, p * sizeof(double), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d.beta, beta0.data(), p * sizeof(double), cudaMemcpyHostToDevice, s));
@@ -1156,22 +1262,43 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
         if (ctx->nranks == 1 && !ctx->per_coordinate_fit) {
             // the whole cycle on the device: one cooperative launch per run of
             // same-kind columns (one launch for an all-indicator design)
+            // (the risk-suffix cycle when the layout allows it and max|eta| is
+            // within its range; the fused-scan cycle otherwise and for the
+            // coordinates the risk-suffix cycle hands back)
             for (const auto& run : ctx->runs) {
                 int32_t done = 0;
                 while (done < run[1]) {
-                    const int izero = 0;
-                    CK(cudaMemcpyAsync(&d.ctl->resume, &izero, sizeof izero, cudaMemcpyHostToDevice, s));
-                    tmark(ctx, 0);
-                    KL(1, launch_cycle(d, ctx->cols_d + run[0] + done, run[1] - done, run[2] != 0, s));
-                    tend(ctx);
-                    if (scx_status st = read_ctl(ctx)) return st;
-                    if (ctx->ctl_h->err_kind) return map_error(ctx, -1);
-                    const int32_t r = ctx->ctl_h->resume;
+                    const ColArgs* cols = ctx->cols_d + run[0] + done;
+                    const int32_t left = run[1] - done;
+                    if (rs_usable(ctx)) {
+                        ctx->rs_stats[0] += 1;
+                        tmark(ctx, 3);
+                        KL(1, launch_rs_cycle(d, cols, left, 0, s));
+                        tend(ctx);
+                        if (scx_status st = read_ctl(ctx)) return st;
+                        if (ctx->ctl_h->err_kind) return map_error(ctx, -1);
+                        done += ctx->ctl_h->resume;
+                        const int why = ctx->ctl_h->rs_reason;
+                        if (why == kRsDone) break;
+                        if (why == kRsRefresh) {
+                            KL(2, launch_refresh(d, s));
+                            if (scx_status st = check_device_error(ctx)) return st;
+                        } else if (why == kRsBound) {
+                            ctx->rs_stats[2] += 1;
+                        } else if (why == kRsExact) {
+                            // this coordinate through the exact fused scan, then resume
+                            ctx->rs_stats[1] += 1;
+                            if (scx_status st = fused_cycle(ctx, ctx->cols_d + run[0] + done, 1, run[2] != 0,
+                                                            nullptr))
+                                return st;
+                            done += 1;
+                        }
+                        continue;  // kRsBound: rs_usable() is now false
+                    }
+                    int32_t r = 0;
+                    if (scx_status st = fused_cycle(ctx, cols, left, run[2] != 0, &r)) return st;
                     if (r <= 0) break;
-                    // 256 accepted updates: refresh eta/D from beta, then resume
                     done += r;
-                    KL(2, launch_refresh(d, s));
-                    if (scx_status st = check_device_error(ctx)) return st;
                 }
             }
         } else {
@@ -1260,7 +1387,7 @@ scx_status scx_timing_reset(scx_ctx* ctx) {
     return SCX_OK;
 }
 scx_status scx_timing_get(scx_ctx* ctx, int kind, double* total_ms, int64_t* launches) {
-    if (!ctx || kind < 0 || kind > 2) return SCX_ERR_VALIDATION;
+    if (!ctx || kind < 0 || kind > 3) return SCX_ERR_VALIDATION;
     tcollect(ctx);
     *total_ms = ctx->timer.ms[kind];
     *launches = ctx->timer.launches[kind];

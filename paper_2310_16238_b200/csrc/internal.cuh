@@ -99,8 +99,19 @@ struct DevCtl {
     double part[4];         // multi-GPU: (local lin, ratio sum, variance sum, 0)
     long long warn_coord[64];
     int resume;     // cycle kernel: coordinates done before it stopped for a refresh (0: ran to the end)
-    int pad3;
+    int rs_reason;  // risk-suffix cycle: why it stopped (RsStop)
 };
+
+// Why a risk-suffix cycle launch returned before its last coordinate.
+enum RsStop : int {
+    kRsDone = 0,      // every coordinate processed
+    kRsRefresh = 1,   // 256 accepted updates: refresh eta/D, then resume
+    kRsExact = 2,     // coordinate `resume`'s g'' cancels against its terms (S1 ~ S0 on
+                      // its risk sets): the per-coordinate fused scan decides
+    kRsBound = 3,     // max|eta| bound passed kRsEtaBound: finish with the fused scan
+};
+constexpr double kRsEtaBound = 300.0;  // w/S0^2 and a*Q*(a+2C) stay in fp64 range below it
+constexpr int kRsMaxStrata = 1024;     // strata of one chunk staged in shared memory
 
 struct Pref1 {
     double v0;
@@ -148,6 +159,20 @@ __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// TMA: 2-D tiled tensor copy shared -> global (bulk group of the issuing thread).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
+        "r"(c0), "r"(c1), "r"(smem_u32(src))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// this thread's bulk groups have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// ... and their global writes are complete
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // TMA: 2-D tiled tensor copy global -> shared, completion on an mbarrier.
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
@@ -241,12 +266,25 @@ struct DesignDev {
     CUtensorMap tmap_D1;      // box 16 x 128 (2048-row K1 tile)
     CUtensorMap tmap_eta;
     int coop_blocks;          // co-resident blocks for the cooperative kernels
+    // risk-suffix CCD cycle (chunk layout only)
+    double* rs_u;             // [npad] scratch: w/S0 per row (forward pass)
+    double* rs_R;             // [npad] within-stratum suffix sum of w/S0 from each row
+    double* rs_Q;             // [npad] within-stratum suffix sum of w/S0^2 from each row
+    CUtensorMap tmap_u;       // box 16 x 256 (4096-row tile), loads and stores
+    CUtensorMap tmap_R;
+    CUtensorMap tmap_Q;
+    int32_t* chunk_k;         // [nchunks+1] first stratum of each chunk
+    int32_t rs_ok;            // chunks hold <= kRsMaxStrata strata each
 };
 
 enum K1Mode : int { kK1Eval = 0, kK1Fit = 1, kK1Diag = 2, kK1Partial = 3 };
 
 cudaError_t launch_k1(const DesignDev& d, const ColArgs& col, int mode, cudaStream_t s);
 cudaError_t k1_trace_copy(long long* out);
+// risk-suffix CCD cycle over cols_d[0..ncols): mode 0 fit, 1 evaluate cols_d[0]
+// only (g, h into ctl), 2 risk prefix only
+cudaError_t launch_rs_cycle(const DesignDev& d, const ColArgs* cols_d, int ncols, int mode,
+                            cudaStream_t s);
 // one CCD cycle in one cooperative launch over cols_d[0..ncols) (all of one
 // kind: indicator or value columns)
 cudaError_t launch_cycle(const DesignDev& d, const ColArgs* cols_d, int ncols, bool indicator,

@@ -197,6 +197,23 @@ class DeviceDesign:
     def stream(self) -> int:
         return int(_lib().scx_stream(self._h) or 0)
 
+    def set_fit_path(self, path: int) -> bool:
+        """CCD cycle implementation: 0 automatic (risk-suffix cycle on the chunked
+        layout), 1 per-coordinate fused scan only. Returns whether the
+        risk-suffix cycle can run on this design."""
+        rs = C.c_int()
+        _check(_lib().scx_set_fit_path(self._h, int(path), C.byref(rs)), self._h)
+        return bool(rs.value)
+
+    def fit_path_stats(self) -> dict:
+        """Counters of the last ccd_fit: risk-suffix cycle launches, coordinates
+        handed to the exact fused scan, |eta|-bound hand-offs, fused-scan cycle
+        launches."""
+        out = (C.c_int64 * 4)()
+        _check(_lib().scx_fit_path_stats(self._h, out), self._h)
+        return dict(risk_suffix_launches=out[0], exact_handoffs=out[1], bound_handoffs=out[2],
+                    fused_scan_launches=out[3])
+
     # -- state residency (one device-resident CoefficientState per context)
     def _activate(self, state: "CoefficientState"):
         if self._state_owner is state:
@@ -303,6 +320,16 @@ def gradient_hessian(dd: DeviceDesign, state: CoefficientState, j: int,
     dd._activate(state)
     g = C.c_double(); h = C.c_double()
     _check(_lib().scx_gradient_hessian(dd.handle, int(j), C.byref(g), C.byref(h)), dd.handle)
+    return GradHess(g.value, h.value)
+
+
+def risk_suffix_gradient_hessian(dd: DeviceDesign, state: CoefficientState, j: int) -> GradHess:
+    """(g', g'') of coordinate j by the risk-suffix formulation the CCD fit runs
+    on the chunked layout (one fused risk scan of the state, then O(nnz_j)
+    gathers); equal to gradient_hessian within rounding."""
+    dd._activate(state)
+    g = C.c_double(); h = C.c_double()
+    _check(_lib().scx_gradient_hessian_rs(dd.handle, int(j), C.byref(g), C.byref(h)), dd.handle)
     return GradHess(g.value, h.value)
 
 

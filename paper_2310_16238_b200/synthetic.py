@@ -168,7 +168,8 @@ def generate(n: int, p: int, k: int, density: float = 0.01, beta_sparsity: float
                       col_ptr=col_ptr.cpu().numpy(), rows=rows_np, true_beta=beta.cpu().numpy(),
                       rows_owner=rows_h)
     del rows_all
-    torch.cuda.synchronize()
+    if dev.type == "cuda":
+        torch.cuda.synchronize()
     torch.cuda.empty_cache()
     out.gen_seconds = time.perf_counter() - t0
     return out
