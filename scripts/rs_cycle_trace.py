@@ -1,0 +1,66 @@
+"""Where a risk-suffix CCD cycle spends its time (SCX_K1_DBG=256).
+
+python scripts/rs_cycle_trace.py [--n 1e7 --p 10000 --k 1000]
+Runs the C4-shaped fit for a few cycles, then one more cycle with the trace on,
+and prints the per-round phase totals (cycles) of CTA 0 for the first 512
+rounds of the last launch: gradient round (eval, barrier+decide), full
+evaluation (eval, barrier+rule), apply, scan.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["SCX_K1_DBG"] = "256"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=float, default=1e7)
+    ap.add_argument("--p", type=int, default=10000)
+    ap.add_argument("--k", type=int, default=1000)
+    ap.add_argument("--cycles", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+    import paper_2310_16238_b200 as sx
+    from paper_2310_16238_b200 import _capi, synthetic
+    lib = _capi.load()
+    syn = synthetic.generate(int(args.n), args.p, args.k, 0.01, seed=11, device="cuda")
+    d = syn.sorted_design()
+    dd = sx.upload(d)
+    gmax = sx.gamma_max(dd)
+    pen = sx.PenaltySpec.shared(args.p, 0.05 * gmax)
+    r = sx.ccd_fit(dd, pen, sx.OptimizerConfig(max_cycles=args.cycles))
+    torch.cuda.synchronize()
+    tr = np.zeros((2, 512, 8), np.int64)
+    lib.scx_debug_k1_trace(tr.ctypes.data_as(C.POINTER(C.c_longlong)))
+    t = tr[1]
+    n = int(np.count_nonzero(t[:, 0]))
+    ph = {"grad_eval": 0, "grad_barrier_decide": 0, "full_eval": 0, "full_barrier_rule": 0,
+          "apply": 0, "scan": 0}
+    nskip = 0
+    for i in range(n):
+        e = t[i]
+        ph["grad_eval"] += e[1] - e[0] if e[1] else 0
+        ph["grad_barrier_decide"] += e[2] - e[1] if e[2] else 0
+        if e[3]:
+            ph["full_eval"] += e[3] - e[2]
+        if e[4]:
+            ph["full_barrier_rule"] += e[4] - e[3]
+        if e[5]:
+            ph["apply"] += e[5] - e[4]
+        if e[6]:
+            ph["scan"] += e[6] - e[5]
+        nskip += int(e[7])
+    tot = int(t[n - 1][6] or t[n - 1][4] or t[n - 1][2]) - int(t[0][0])
+    print(f"rounds={n} skipped={nskip} total_cycles={tot} ({tot / 1.965e3:.0f} us)")
+    for k, v in ph.items():
+        print(f"  {k:22s} {int(v):>10d} cycles {int(v) / max(1, n):8.0f}/round  {v / max(1, tot):.1%}")
+    print("stats", dd.fit_path_stats(), "cycles", r.cycles_used)
+
+
+if __name__ == "__main__":
+    main()

@@ -11,7 +11,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["SCX_K1_DBG"] = "32"
+os.environ["SCX_K1_DBG"] = os.environ.get("SCX_K1_DBG", "32")
 
 
 def main():
@@ -28,23 +28,12 @@ def main():
     tr = np.zeros((2, 512, 8), np.int64)
     lib.scx_debug_k1_trace(tr.ctypes.data_as(C.POINTER(C.c_longlong)))
     t = tr[0]
-    out = {}
-    for pas in (0, 1):
-        rows = []
-        for i in range(64):
-            e = t[pas * 64 + i]
-            if e[0] == 0:
-                break
-            rows.append([int(e[1] - e[0]), int(e[2] - e[1]), int(e[3] - e[2]), int(e[4] - e[3]),
-                         int(e[5] - e[4]), int(e[0] - t[pas * 64 + i - 1][5]) if i else 0])
-        out["fwd" if pas == 0 else "bwd"] = rows
-        tot = int(t[pas * 64 + len(rows) - 1][5] - t[pas * 64][0])
-        out[("fwd" if pas == 0 else "bwd") + "_total_cycles"] = tot
-    print("columns: wait, pass1, blockscan, perrow+smem+sync, writeout, gap_from_prev")
     base = t[0][0]
-    for k in list(range(0, 4)) + list(range(64, 84)):
-        print(k, [int(x - base) if x else 0 for x in t[k][:6]])
-    print(json.dumps(out))
+    print("group-0 forward tiles: [wait_start, data_ready, pass1_done, scan_done, carry_ready, perrow_done, stored] (cycles from start)")
+    for k in range(20):
+        if t[k][0] == 0:
+            break
+        print(k, [int(x - base) if x else 0 for x in t[k][:7]])
 
 
 if __name__ == "__main__":
