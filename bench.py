@@ -529,9 +529,9 @@ def main():
     if rs is not None:
         roof = {"bound": "hbm", "achieved": rs["gbs"], "peak": hbm_peak, "unit": "GB/s",
                 "frac": rs["gbs"] / hbm_peak,
-                "traffic": ncu_traffic("ncu_rs_prefix_summary.json", design.n_rows),
-                "kernel": "k_rs_cycle risk prefix (fused segmented scan of D -> w/S0, w/S0^2 "
-                          "-> within-stratum prefixes)",
+                "traffic": ncu_traffic("ncu_rs_scan_summary.json", design.n_rows),
+                "kernel": "k_rs_cycle risk scan (forward stratum-segmented S0 -> u = w/S0; "
+                          "backward within-stratum suffix sums R of u and Q of u^2/w)",
                 "algorithmic_bytes_per_launch": rs["bytes"],
                 "algorithmic_bytes_per_row": row_bytes_rs,
                 "avg_launch_ms": rs["ms"], "peak_source": peak_src}

@@ -736,8 +736,8 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     d.offsets = ctx->offsets_d;
     if (!make_tmap(&d.tmap_D, d.D, d.npad) || !make_tmap(&d.tmap_eta, d.eta, d.npad) ||
         !make_tmap(&d.tmap_D1, d.D, d.npad, kK1TileRows) ||
-        (d.rs_ok && (!make_tmap(&d.tmap_u, d.rs_u, d.npad, kK1TileRows) || !make_tmap(&d.tmap_R, d.rs_R, d.npad) ||
-                     !make_tmap(&d.tmap_Q, d.rs_Q, d.npad))))
+        (d.rs_ok && (!make_tmap(&d.tmap_u, d.rs_u, d.npad, kK1TileRows) || !make_tmap(&d.tmap_R, d.rs_R, d.npad, kK1TileRows) ||
+                     !make_tmap(&d.tmap_Q, d.rs_Q, d.npad, kK1TileRows))))
         return fail(ctx, SCX_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 
     // co-resident block count for the cooperative kernels

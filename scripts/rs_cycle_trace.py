@@ -38,12 +38,16 @@ def main():
     tr = np.zeros((2, 512, 8), np.int64)
     lib.scx_debug_k1_trace(tr.ctypes.data_as(C.POINTER(C.c_longlong)))
     t = tr[1]
-    n = int(np.count_nonzero(t[:, 0]))
+    # rounds of the last launch (the kernel clears the trace at launch); the
+    # round index counts grid reductions, so full evaluations leave gaps
+    n = int(np.max(np.nonzero(t[:, 0])[0])) + 1 if t[:, 0].any() else 0
     ph = {"grad_eval": 0, "grad_barrier_decide": 0, "full_eval": 0, "full_barrier_rule": 0,
           "apply": 0, "scan": 0}
     nskip = 0
     for i in range(n):
         e = t[i]
+        if not e[0]:
+            continue
         ph["grad_eval"] += e[1] - e[0] if e[1] else 0
         ph["grad_barrier_decide"] += e[2] - e[1] if e[2] else 0
         if e[3]:
