@@ -157,3 +157,26 @@ def test_risk_suffix_bound_hands_over(oracle, ref):
     assert r.cycles_used == want["cycles"]
     assert np.max(np.abs(r.beta - want["beta"])) <= BETA_ATOL
     assert np.allclose(r.objective_trace, want["trace"], rtol=LL_RTOL, atol=0)
+
+
+def test_risk_suffix_mixed_penalties_match_oracle(oracle, ref):
+    """Per-coordinate penalties mixing unpenalised (gamma = 0), weak and strong L1
+    weights, so gradient rounds stop at coordinates that cannot be skipped
+    (beta != 0 or gamma = 0) at every position of a round, and rounds of skipped
+    coordinates alternate with full evaluations. Fit vs oracle."""
+    n, k, p = 1_200_000, 1200, 16
+    a = _design(oracle, ref, n, k, p, 0.03, 1e9, False, 4242)
+    d = oracle.design(a)
+    dd = upload(a, values=False)
+    assert dd.set_fit_path(0)
+    gmax = sx.gamma_max(dd)
+    frac = np.array([0.0, 0.3, 0.02, 0.5, 0.0, 0.01, 0.9, 0.05,
+                     0.2, 0.0, 0.6, 0.03, 0.4, 0.08, 0.0, 0.7])
+    gamma = frac * gmax
+    want = oracle.ccd_fit(d, gamma, max_cycles=40, tol=1e-8)
+    r = sx.ccd_fit(dd, sx.PenaltySpec(gamma), sx.OptimizerConfig(max_cycles=40, tolerance=1e-8))
+    assert r.cycles_used == want["cycles"]
+    assert np.max(np.abs(r.beta - want["beta"])) <= BETA_ATOL
+    assert np.allclose(r.objective_trace, want["trace"], rtol=LL_RTOL, atol=0)
+    nz = np.count_nonzero(r.beta)
+    assert 0 < nz < p, nz  # both kinds of coordinate present at the optimum
