@@ -164,7 +164,7 @@ def test_risk_suffix_mixed_penalties_match_oracle(oracle, ref):
     weights, so gradient rounds stop at coordinates that cannot be skipped
     (beta != 0 or gamma = 0) at every position of a round, and rounds of skipped
     coordinates alternate with full evaluations. Fit vs oracle."""
-    n, k, p = 1_200_000, 1200, 16
+    n, k, p = 1_300_000, 1300, 16
     a = _design(oracle, ref, n, k, p, 0.03, 1e9, False, 4242)
     d = oracle.design(a)
     dd = upload(a, values=False)
