@@ -29,11 +29,11 @@ $(OBJDIR)/capi.o: $(CSRC)/capi.cu $(CSRC)/internal.cuh $(CSRC)/rules.cuh include
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/capi.ptxas.txt || (cat $(OBJDIR)/capi.ptxas.txt; exit 1)
 
-$(OBJDIR)/cv.o: $(CSRC)/cv.cu include/stratcox_b200.h
+$(OBJDIR)/cv.o: $(CSRC)/cv.cu $(CSRC)/internal.cuh include/stratcox_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/cv.ptxas.txt || (cat $(OBJDIR)/cv.ptxas.txt; exit 1)
 
-$(OBJDIR)/transforms.o: $(CSRC)/transforms.cu include/stratcox_b200.h
+$(OBJDIR)/transforms.o: $(CSRC)/transforms.cu $(CSRC)/internal.cuh include/stratcox_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/transforms.ptxas.txt || (cat $(OBJDIR)/transforms.ptxas.txt; exit 1)
 
@@ -42,7 +42,7 @@ $(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o $(OBJDIR)/transforms
 
 oracle:
 	$(MAKE) -C oracle oracle
-	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; else echo "reference absent: using prebuilt oracle/_ref if any"; fi
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref && $(MAKE) -C oracle dropin; else echo "reference absent: using prebuilt oracle/_ref if any"; fi
 
 clean:
 	rm -rf build $(LIB)

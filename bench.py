@@ -112,6 +112,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ---------------------------------------------------------------- CPU reference arm
 def reference_sample(n, p_sample, k, density, seed, threads):
     """Bounded sample of the C4 workload on the reference (oracle/_ref)."""
@@ -334,6 +345,80 @@ def run_small_config(args):
     print(json.dumps(line), flush=True)
 
 
+PARITY_P = 64
+
+
+def cpu_baseline_and_parity(args, sx, gpu_evals):
+    from oracle.oracle_py import Ref
+    from oracle.oracle_py import to_sorted_design
+
+    threads = os.cpu_count() or 1
+    ref = Ref()
+    t0 = time.perf_counter()
+    ds = ref.simulate(args.n, PARITY_P, args.density, 0.8, args.k, 0.3, 11)
+    h, a = ref.build_design(ds)
+    del ds
+    gmax = ref.gamma_max(h, workers=threads)
+    setup = time.perf_counter() - t0
+    gamma = 0.05 * gmax
+    # (i) per-coordinate CCD iteration, run_benchmark semantics (benchmark.cpp:27-41, 71-98)
+    per = ref.time_iterations(h, gamma, 3, args.ref_sweep, threads)
+    cv = 1.0 / float(np.median(per))
+    per1 = ref.time_iterations(h, gamma, 2, 2, 1)
+    cv1 = 1.0 / float(np.median(per1))
+    # (ii) a complete reference ccd_fit of the sample (default OptimizerConfig)
+    gvec = np.full(PARITY_P, gamma)
+    t0 = time.perf_counter()
+    rf = ref.ccd_fit(h, gvec, PARITY_P, workers=threads)
+    ref_fit_s = time.perf_counter() - t0
+    ref.free_design(h)
+    nzc = int(np.count_nonzero(np.diff(a["col_ptr"])))
+    ref_fit_evals = rf["cycles"] * nzc
+    # the library on the same design, same penalty, same path as the timed fits
+    dd = sx.upload(to_sorted_design(a))
+    del a
+    rs_on = dd.set_fit_path(0)
+    gmax_gpu = sx.gamma_max(dd)
+    rg = sx.ccd_fit(dd, sx.PenaltySpec(gvec), sx.OptimizerConfig())
+    stats = dd.fit_path_stats()
+    dd.close()
+    db = np.abs(rg.beta - rf["beta"])
+    trace_rel = float(np.max(np.abs(np.asarray(rg.objective_trace) - rf["trace"]) /
+                             np.maximum(1.0, np.abs(rf["trace"])))) \
+        if len(rg.objective_trace) == len(rf["trace"]) else None
+    parity = {
+        "design": (f"reference simulate(): N={args.n}, K={args.k}, density {args.density}, "
+                   f"p={PARITY_P}, seed 11; L1 at 0.05*gamma_max, default OptimizerConfig"),
+        "reference_cycles": rf["cycles"], "gpu_cycles": rg.cycles_used,
+        "reference_converged": rf["converged"], "gpu_converged": rg.converged,
+        "max_abs_dbeta": float(db.max()), "beta_atol": 1e-8,
+        "supports_equal": bool(np.array_equal(rg.beta != 0, rf["beta"] != 0)),
+        "nonzero": int(np.count_nonzero(rf["beta"])),
+        "max_rel_dtrace": trace_rel, "gamma_max_rel_diff": abs(gmax_gpu - gmax) / abs(gmax),
+        "gpu_fit_path": "risk-suffix cycle" if rs_on else "fused-scan cycle",
+        "gpu_fit_path_stats": stats,
+        "pass": bool(rg.cycles_used == rf["cycles"] and float(db.max()) <= 1e-8 and
+                     np.array_equal(rg.beta != 0, rf["beta"] != 0)),
+        "at_scale_test": "tests/test_large_fit.py (p=200 fit to convergence, C2/C3 at 1e6 "
+                         "subjects); profiles/r02_parity_c4_full.json (p=1e4, 2 cycles)",
+    }
+    cpu = {"value": cv, "unit": "evals/s", "cores": threads, "kind": "reference",
+           "cpu_model": cpu_model(), "value_1thread": cv1,
+           "sample": (f"oracle/_ref (unmodified stratcox, -O3 -fopenmp) on its own simulate() "
+                      f"at N={args.n}, K={args.k}, density {args.density}, {PARITY_P} "
+                      f"covariates: median of 3 sweeps x {args.ref_sweep} CCD coordinate "
+                      f"iterations at gamma=0.05*gamma_max (benchmark.cpp:27-41), {threads} "
+                      f"threads; 1 thread: 2 x 2 iterations; setup {setup:.1f}s excluded"),
+           "reference_fit": {"p": PARITY_P, "seconds": ref_fit_s, "cycles": rf["cycles"],
+                             "evals": ref_fit_evals,
+                             "evals_per_s_in_fit": ref_fit_evals / ref_fit_s},
+           "fit_wall_s_extrapolated": float(np.mean(gpu_evals)) / cv,
+           "extrapolation": ("C4 GPU fit's coordinate evaluations / the reference's "
+                             "per-evaluation rate; the same design's reference ccd_fit above "
+                             "checks that rate inside a complete fit")}
+    return cpu, parity
+
+
 # ---------------------------------------------------------------- GPU arm
 def flush_l2(buf):
     buf.add_(1)
@@ -359,6 +444,9 @@ def main():
                     help="BASELINE config: c4 (default, the headline) or c1-c3 (one line each)")
     args = ap.parse_args()
 
+    for knob in ("SCX_K1_DBG", "SCX_FIT_PER_COORD"):
+        if os.environ.get(knob, "0") not in ("", "0"):
+            raise SystemExit(f"bench.py: {knob} is a diagnostic knob and must be unset")
     if args.config != "c4":
         run_small_config(args)
         return
@@ -577,22 +665,18 @@ def main():
         dd2.close()
     e2e_value = (float(np.mean(e2e_evals)) / float(np.mean(e2e_times))) if e2e_times else None
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline + parity of the benchmarked fit path (rank 0, N=1 only).
+    # The reference (oracle/_ref) generates a bounded sample of the same workload
+    # with its own simulate() (N, K, density of C4; PARITY_P covariates), times
+    # its per-coordinate CCD iteration with all host threads and with one, and
+    # runs a complete reference ccd_fit on it; the library then fits the SAME
+    # design (uploaded from the reference's SortedDesign) through the same
+    # risk-suffix path the timed fits use, and the two fits are compared.
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            ref, rh, rgamma, setup = reference_sample(args.n, 32, args.k, args.density, 11,
-                                                      threads)
-            per = ref.time_iterations(rh, rgamma, 3, args.ref_sweep, threads)
-            cv = 1.0 / float(np.median(per))
-            cpu = {"value": cv, "unit": "evals/s", "cores": threads, "kind": "reference",
-                   "sample": (f"oracle/_ref (unmodified stratcox, -O3 -fopenmp) on N={args.n}, "
-                              f"K={args.k}, density {args.density}, 32 covariates: median of 3 "
-                              f"sweeps x {args.ref_sweep} CCD coordinate iterations "
-                              f"(benchmark.cpp:27-41); setup {setup:.1f}s excluded"),
-                   "fit_wall_s_extrapolated": float(np.mean(evals)) / cv}
-            ref.free_design(rh)
+            cpu, parity = cpu_baseline_and_parity(args, sx, evals)
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -629,6 +713,7 @@ def main():
             "fit_path": "risk-suffix cycle" if rs_on else "fused-scan cycle",
             "fit_path_stats": path_stats,
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "seconds_per_step": float(np.mean(e2e_times)) if e2e_times else None},

@@ -156,7 +156,8 @@ typedef struct {
     int32_t trace_len;       /* entries written */
     int32_t cycles_used;     /* FitResult::cycles_used */
     int32_t converged;       /* FitResult::converged */
-    int32_t n_warnings;      /* coordinates skipped after 10 halvings */
+    int32_t n_warnings;      /* coordinates skipped after 10 halvings (exact count; the first
+                                min(warning_cap, 65536) are listed in warning_coords) */
     int64_t* warning_coords; /* [warning_cap] coordinate of each warning, in order (may be NULL) */
     int32_t warning_cap;
     uint32_t updates_since_refresh;

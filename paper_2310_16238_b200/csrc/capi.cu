@@ -55,7 +55,7 @@ struct NcclApi {
     }
 };
 NcclApi g_nccl;
-constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclMax = 2;
+constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2;
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -107,6 +107,7 @@ struct scx_ctx {
     bool has_design = false;
     DesignDev d{};
     DevCtl* ctl_h = nullptr;  // pinned mirror of d.ctl
+    long long* warn_d = nullptr;  // [kWarnCap] fit warnings (DevCtl::warn_coord)
     // host metadata
     std::vector<ColArgs> cols;
     std::vector<int32_t> zero_cols;
@@ -136,6 +137,7 @@ struct scx_ctx {
     void* comm = nullptr;
     int nranks = 1, rank = 0;
     double* parts_d = nullptr;  // [nranks][4]
+    std::vector<uint8_t> gnz;   // column has entries on SOME rank (the sharded loop's column set)
     Timer timer;
     int64_t launches = 0;  // kernels launched by this context
 };
@@ -496,6 +498,7 @@ scx_status scx_create(int device, scx_ctx** out) {
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc((void**)&ctx->d.ctl, sizeof(DevCtl)) != cudaSuccess ||
         cudaMallocHost((void**)&ctx->ctl_h, sizeof(DevCtl)) != cudaSuccess ||
+        cudaMalloc((void**)&ctx->warn_d, kWarnCap * sizeof(long long)) != cudaSuccess ||
         cudaMalloc((void**)&ctx->out2, 4 * sizeof(double)) != cudaSuccess) {
         delete ctx;
         return SCX_ERR_CUDA;
@@ -504,6 +507,8 @@ scx_status scx_create(int device, scx_ctx** out) {
     memset(&init, 0, sizeof init);
     init.epoch = 1;
     init.bad_min = kNoRow;
+    init.warn_coord = ctx->warn_d;
+    init.warn_cap = kWarnCap;
     cudaMemcpy(ctx->d.ctl, &init, sizeof init, cudaMemcpyHostToDevice);
     *out = ctx;
     return SCX_OK;
@@ -516,6 +521,7 @@ void scx_destroy(scx_ctx* ctx) {
     free_design(ctx);
     if (ctx->d.ctl) cudaFree(ctx->d.ctl);
     if (ctx->out2) cudaFree(ctx->out2);
+    if (ctx->warn_d) cudaFree(ctx->warn_d);
     if (ctx->ctl_h) cudaFreeHost(ctx->ctl_h);
     for (auto e : ctx->timer.ev) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1304,7 +1310,10 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
         } else {
             for (int64_t j = 0; j < p; ++j) {
                 const ColArgs& col = ctx->cols[j];
-                if (col.nnz == 0) continue;
+                // every rank walks the same (globally non-empty) columns, so the
+                // collectives of run_coordinate pair up; a rank without local
+                // rows joins with zero partials
+                if (ctx->nranks > 1 ? !ctx->gnz[j] : col.nnz == 0) continue;
                 if (scx_status st = run_coordinate(ctx, col)) return st;
             }
         }
@@ -1334,9 +1343,12 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
     res->n_warnings = ctx->ctl_h->n_warn;
     res->updates_since_refresh = ctx->ctl_h->updates;
     res->n_evaluations = ctx->ctl_h->n_eval;
-    if (res->warning_coords)
-        for (int w = 0; w < std::min(res->n_warnings, std::min(res->warning_cap, 64)); ++w)
-            res->warning_coords[w] = ctx->ctl_h->warn_coord[w];
+    if (res->warning_coords && res->n_warnings > 0 && res->warning_cap > 0) {
+        const int nw = std::min(res->n_warnings, std::min(res->warning_cap, kWarnCap));
+        std::vector<long long> w(nw);
+        CK(cudaMemcpy(w.data(), ctx->warn_d, nw * sizeof(long long), cudaMemcpyDeviceToHost));
+        for (int q = 0; q < nw; ++q) res->warning_coords[q] = w[q];
+    }
     return SCX_OK;
 }
 
@@ -1430,8 +1442,31 @@ scx_status scx_comm_init(scx_ctx* ctx, int nranks, int rank, const char unique_i
         CK(cudaMemcpyAsync(xm.data(), xm_d, xm.size() * sizeof(double), cudaMemcpyDeviceToHost,
                            ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(xm_d);
         for (int64_t j = 0; j < ctx->d.p; ++j) ctx->cols[j].xmax = xm[j];
+        // which columns have entries on some rank: the global column set, the
+        // same on every rank (zero columns: trust halving at the cycle end)
+        for (int64_t j = 0; j < ctx->d.p; ++j) xm[j] = (double)ctx->cols[j].nnz;
+        CK(cudaMemcpyAsync(xm_d, xm.data(), xm.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        if (g_nccl.AllReduce(xm_d, xm_d, ctx->d.p, kNcclFloat64, kNcclSum, comm, ctx->stream) != 0)
+            return fail(ctx, SCX_ERR_CUDA, "ncclAllReduce failed");
+        CK(cudaMemcpyAsync(xm.data(), xm_d, xm.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(xm_d);
+        ctx->gnz.assign(ctx->d.p, 0);
+        ctx->zero_cols.clear();
+        for (int64_t j = 0; j < ctx->d.p; ++j) {
+            ctx->gnz[j] = xm[j] > 0.0;
+            if (!ctx->gnz[j]) ctx->zero_cols.push_back((int32_t)j);
+        }
+        if (ctx->zero_cols_d) cudaFree(ctx->zero_cols_d);
+        CK(dmalloc(&ctx->zero_cols_d, ctx->zero_cols.size()));
+        if (!ctx->zero_cols.empty())
+            CK(cudaMemcpyAsync(ctx->zero_cols_d, ctx->zero_cols.data(),
+                               ctx->zero_cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                               ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     return SCX_OK;
 }
@@ -1442,6 +1477,7 @@ scx_status scx_comm_destroy(scx_ctx* ctx) {
     ctx->comm = nullptr;
     ctx->nranks = 1;
     ctx->rank = 0;
+    ctx->gnz.clear();
     return SCX_OK;
 }
 

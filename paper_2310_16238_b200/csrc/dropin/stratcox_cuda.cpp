@@ -10,9 +10,13 @@
 // Contexts: one scx_ctx per calling thread (thread_local), because the
 // reference calls ccd_fit concurrently from OpenMP threads
 // (proj/src/resample.cpp:121,207). The uploaded design is cached per thread
-// and keyed by the design object's identity (address, storage pointers and
-// shape); a CoefficientState passed by the caller is uploaded per call
-// (parity boundary), while ccd_fit keeps its whole loop on the device.
+// and keyed by a 64-bit hash of its CONTENT (offsets, tie ends, events, times
+// and every column's rows and values) plus its shape: the reference builds a
+// stack-local SortedDesign per bootstrap replicate and per fold
+// (resample.cpp:129-130,218-219), so an address can be reused by a different
+// design of the same shape and identity alone would return a stale upload. A
+// CoefficientState passed by the caller is uploaded per call (parity
+// boundary), while ccd_fit keeps its whole loop on the device.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -35,9 +39,8 @@ namespace {
 
 struct ThreadCtx {
     scx_ctx* h = nullptr;
-    const SortedDesign* design = nullptr;
-    const void* time_ptr = nullptr;
-    const void* cols_ptr = nullptr;
+    bool valid = false;
+    uint64_t hash = 0;
     std::size_t n = 0, p = 0, nnz = 0;
     ~ThreadCtx() {
         if (h) scx_destroy(h);
@@ -74,12 +77,58 @@ void check_rule(scx_status s) {
     if (s != SCX_OK) raise(s, scx_rule_error());
 }
 
+// 64-bit content hash: four independent multiply-rotate lanes over 8-byte
+// words (a tail is zero-padded), folded with the byte count.
+struct Hasher {
+    uint64_t a = 0x9e3779b97f4a7c15ull, b = 0xc2b2ae3d27d4eb4full, c = 0x165667b19e3779f9ull,
+             e = 0x27d4eb2f165667c5ull;
+    uint64_t bytes = 0;
+    static uint64_t mix(uint64_t h, uint64_t w) {
+        h ^= w * 0x87c37b91114253d5ull;
+        h = (h << 31) | (h >> 33);
+        return h * 0x4cf5ad432745937full + 0x52dce729ull;
+    }
+    void add(const void* p, std::size_t nbytes) {
+        const unsigned char* s = static_cast<const unsigned char*>(p);
+        std::size_t i = 0;
+        for (; i + 32 <= nbytes; i += 32) {
+            uint64_t w[4];
+            std::memcpy(w, s + i, 32);
+            a = mix(a, w[0]);
+            b = mix(b, w[1]);
+            c = mix(c, w[2]);
+            e = mix(e, w[3]);
+        }
+        for (; i < nbytes; i += 8) {
+            uint64_t w = 0;
+            std::memcpy(&w, s + i, std::min<std::size_t>(8, nbytes - i));
+            a = mix(a, w);
+        }
+        bytes += nbytes;
+        b = mix(b, nbytes);
+    }
+    uint64_t value() const { return mix(mix(mix(mix(a, b), c), e), bytes); }
+};
+
+uint64_t content_hash(const SortedDesign& d) {
+    Hasher h;
+    h.add(d.stratum_offsets.data(), d.stratum_offsets.size() * sizeof(d.stratum_offsets[0]));
+    h.add(d.tie_group_end.data(), d.tie_group_end.size() * sizeof(d.tie_group_end[0]));
+    h.add(d.data.event.data(), d.data.event.size() * sizeof(d.data.event[0]));
+    h.add(d.data.time.data(), d.data.time.size() * sizeof(d.data.time[0]));
+    for (const auto& c : d.data.columns) {
+        h.add(c.rows.data(), c.rows.size() * sizeof(c.rows[0]));
+        h.add(c.values.data(), c.values.size() * sizeof(c.values[0]));
+    }
+    return h.value();
+}
+
 scx_ctx* ctx_for(const SortedDesign& d) {
     std::size_t nnz = 0;
     for (const auto& c : d.data.columns) nnz += c.nnz();
+    const uint64_t hash = content_hash(d);
     ThreadCtx& t = g_ctx;
-    if (t.h && t.design == &d && t.time_ptr == d.data.time.data() &&
-        t.cols_ptr == d.data.columns.data() && t.n == d.n_rows() && t.p == d.n_covariates() &&
+    if (t.h && t.valid && t.hash == hash && t.n == d.n_rows() && t.p == d.n_covariates() &&
         t.nnz == nnz)
         return t.h;
     if (!t.h) {
@@ -99,15 +148,14 @@ scx_ctx* ctx_for(const SortedDesign& d) {
         values.insert(values.end(), c.values.begin(), c.values.end());
         col_ptr[j + 1] = static_cast<int64_t>(rows.size());
     }
-    t.design = nullptr;
+    t.valid = false;
     check(scx_upload_design(t.h, static_cast<int64_t>(d.n_rows()), d.n_strata(),
                             d.stratum_offsets.data(), d.data.event.data(), d.tie_group_end.data(),
                             static_cast<int64_t>(d.n_covariates()), col_ptr.data(), rows.data(),
                             values.data()),
           &d);
-    t.design = &d;
-    t.time_ptr = d.data.time.data();
-    t.cols_ptr = d.data.columns.data();
+    t.valid = true;
+    t.hash = hash;
     t.n = d.n_rows();
     t.p = d.n_covariates();
     t.nnz = nnz;
@@ -361,7 +409,7 @@ FitResult run_fit(const SortedDesign& design, const PenaltySpec& penalty,
     r.beta.assign(p, 0.0);
     r.trust.assign(p, 0.0);
     std::vector<double> trace(static_cast<std::size_t>(std::max(1, config.max_cycles)) + 1);
-    std::vector<int64_t> warn(64);
+    std::vector<int64_t> warn(1 << 16);  // kWarnCap
     scx_fit_options opt{config.max_cycles, config.tolerance, config.initial_trust};
     scx_fit_result out{};
     out.beta = r.beta.data();

@@ -97,7 +97,9 @@ struct DevCtl {
     int n_warn;             // coordinates skipped after 10 halvings
     long long n_eval;       // gradient/Hessian evaluations
     double part[4];         // multi-GPU: (local lin, ratio sum, variance sum, 0)
-    long long warn_coord[64];
+    long long* warn_coord;  // [warn_cap] coordinate of each warning, in order (device buffer)
+    int warn_cap;
+    int pad3;
     int resume;     // cycle kernel: coordinates done before it stopped for a refresh (0: ran to the end)
     int rs_reason;  // risk-suffix cycle: why it stopped (RsStop)
 };
@@ -111,6 +113,7 @@ enum RsStop : int {
     kRsBound = 3,     // max|eta| bound passed kRsEtaBound: finish with the fused scan
 };
 constexpr double kRsEtaBound = 300.0;  // w/S0^2 and a*Q*(a+2C) stay in fp64 range below it
+constexpr int kWarnCap = 1 << 16;     // warnings recorded per fit (the count is exact)
 constexpr int kRsMaxStrata = 1024;     // strata of one chunk staged in shared memory
 
 struct Pref1 {

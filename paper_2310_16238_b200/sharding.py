@@ -103,9 +103,14 @@ def init_comm(dd, group=None):
     if rank == 0:
         if lib.scx_comm_unique_id(buf) != 0:
             raise RuntimeError("scx_comm_unique_id failed (libnccl.so.2 missing?)")
-    t = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
+    # an NCCL process group only moves CUDA tensors; gloo takes CPU ones
+    if dist.get_backend(group) == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
+    else:
+        dev = torch.device("cpu")
+    t = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone().to(dev)
     dist.broadcast(t, src=0, group=group)
-    raw = bytes(t.tolist())
+    raw = bytes(t.cpu().tolist())
     rc = lib.scx_comm_init(dd.handle, world, rank, raw)
     if rc != 0:
         raise RuntimeError(lib.scx_last_error(dd.handle).decode())

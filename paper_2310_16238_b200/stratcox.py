@@ -495,7 +495,7 @@ def ccd_fit(dd: DeviceDesign, penalty: PenaltySpec, config: Optional[OptimizerCo
     beta = np.zeros(p, np.float64)
     trust = np.zeros(p, np.float64)
     trace = np.zeros(max(1, config.max_cycles) + 1, np.float64)
-    wcap = 64
+    wcap = 1 << 16  # kWarnCap: the library records this many; n_warnings is exact
     wc = np.zeros(wcap, np.int64)
     res = _capi.FitResultC(ptr(beta, C.c_double), ptr(trust, C.c_double), ptr(trace, C.c_double),
                            0, 0, 0, 0, ptr(wc, C.c_int64), wcap, 0, 0)
@@ -509,6 +509,8 @@ def ccd_fit(dd: DeviceDesign, penalty: PenaltySpec, config: Optional[OptimizerCo
                               ptr(ib, C.c_double), C.byref(res)), dd.handle)
     warnings = [f"coordinate {dd.design.covariate_name(int(j))} skipped: step overflow persisted "
                 f"after 10 halvings" for j in wc[:min(res.n_warnings, wcap)]]
+    if res.n_warnings > wcap:
+        warnings.append(f"... {res.n_warnings - wcap} more step-overflow warnings not recorded")
     return FitResult(beta=beta, objective_trace=list(trace[:res.trace_len]),
                      cycles_used=int(res.cycles_used), converged=bool(res.converged),
                      trust=trust, warnings=warnings, n_evaluations=int(res.n_evaluations),
