@@ -40,7 +40,7 @@ $(OBJDIR)/transforms.o: $(CSRC)/transforms.cu $(CSRC)/internal.cuh include/strat
 $(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o $(OBJDIR)/transforms.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
-oracle:
+oracle: lib
 	$(MAKE) -C oracle oracle
 	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref && $(MAKE) -C oracle dropin; else echo "reference absent: using prebuilt oracle/_ref if any"; fi
 

@@ -140,6 +140,13 @@ scx_status scx_apply_trust_region(double proposed, double trust, double* applied
 scx_status scx_l1_coordinate_update(double g1, double g2, double beta_j, double gamma_j,
                                     double* step, int* skipped, int* flat);
 
+/* Elastic-net rule (EXTENSION, no reference counterpart; BASELINE config 1's
+ * "L2 prior"): the ridge term l2_j beta_j^2 / 2 adds l2_j beta_j to g' and l2_j
+ * to g'', then l1_coordinate_update (optimizer.cpp:51-78) runs on the
+ * penalised pair. l2_j = 0 is scx_l1_coordinate_update exactly. */
+scx_status scx_coordinate_update(double g1, double g2, double beta_j, double gamma_j, double l2_j,
+                                 double* step, int* skipped, int* flat);
+
 /* Message of the last failing scalar-rule call on this thread. */
 const char* scx_rule_error(void);
 
@@ -169,6 +176,16 @@ typedef struct {
  * synchronises once per cycle (objective, max step, error word). */
 scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options* options,
                        const double* initial_beta, scx_fit_result* result);
+
+/* ccd_fit with an optional L2 (ridge / Gaussian) prior l2[p] >= 0 (NULL: none,
+ * = scx_ccd_fit). EXTENSION, no reference counterpart: the objective becomes
+ * -log L + sum gamma_j |beta_j| + sum l2_j beta_j^2 / 2 and every coordinate
+ * uses scx_coordinate_update's rule. Parity unpinned against the reference
+ * (it has no L2 prior); checked by KKT conditions and against the oracle's
+ * restatement of the same rule. */
+scx_status scx_ccd_fit_prior(scx_ctx* ctx, const double* gamma, const double* l2,
+                             const scx_fit_options* options, const double* initial_beta,
+                             scx_fit_result* result);
 
 /* gamma_max (resample.hpp:38-39, resample.cpp:42-55) with a penalty template
  * gamma_template[p] (NULL = every coefficient penalized). */

@@ -401,6 +401,10 @@ class Oracle:
                                                    _d, _ip, _ip]),
             "orc_ccd_fit": (C.c_int, [D, _d, C.c_int, C.c_double, C.c_double, C.c_int64, _d, _d,
                                       _d, _ip, _ip, _ip, _d, _ip]),
+            "orc_ccd_fit_prior": (C.c_int, [D, _d, _d, C.c_int, C.c_double, C.c_double,
+                                            C.c_int64, _d, _d, _d, _ip, _ip, _ip, _d, _ip]),
+            "orc_coordinate_update": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double,
+                                                C.c_double, _d, _ip, _ip]),
             "orc_gamma_max": (C.c_int, [D, C.c_int64, _d]),
         }
         for name, (res, args) in sig.items():
@@ -511,14 +515,24 @@ class Oracle:
                                                   C.byref(f)))
         return s.value, bool(sk.value), bool(f.value)
 
+    def coordinate_update(self, g1, g2, b, gm, lam):
+        s = C.c_double(); sk = C.c_int(); f = C.c_int()
+        self._chk(self.L.orc_coordinate_update(g1, g2, b, gm, lam, C.byref(s), C.byref(sk),
+                                               C.byref(f)))
+        return s.value, bool(sk.value), bool(f.value)
+
     def ccd_fit(self, d, gamma, max_cycles=1000, tol=1e-6, initial_trust=1.0, chunk=4096,
-                initial_beta=None):
+                initial_beta=None, l2=None):
+        """l2: optional per-coefficient L2 prior weights (extension, not in the
+        reference; see orc_ccd_fit_prior)."""
         p = d.p
         beta = np.empty(p); trace = np.empty(max_cycles + 1); trust = np.empty(p)
         tl = C.c_int(); cy = C.c_int(); cv = C.c_int(); nw = C.c_int()
         g = np.ascontiguousarray(gamma, np.float64)
+        lam = None if l2 is None else np.ascontiguousarray(l2, np.float64)
         ib = None if initial_beta is None else np.ascontiguousarray(initial_beta, np.float64)
-        self._chk(self.L.orc_ccd_fit(C.byref(d), _p(g, C.c_double), max_cycles, tol,
+        self._chk(self.L.orc_ccd_fit_prior(C.byref(d), _p(g, C.c_double), _p(lam, C.c_double),
+                                     max_cycles, tol,
                                      initial_trust, chunk, _p(ib, C.c_double),
                                      _p(beta, C.c_double), _p(trace, C.c_double), C.byref(tl),
                                      C.byref(cy), C.byref(cv), _p(trust, C.c_double),

@@ -556,11 +556,25 @@ int orc_l1_coordinate_update(double g1, double g2, double beta_j, double gamma_j
     return rc;
 }
 
-/* PenaltySpec::value, optimizer.cpp:18-22 */
-static double penalty_value(const double* gamma, const double* beta, int64_t p) {
+/* PenaltySpec::value, optimizer.cpp:18-22; with an L2 (ridge / Gaussian)
+ * prior l2 (NOT in the reference: BASELINE config 1's "L2 prior", parity
+ * unpinned) the value adds sum_j l2_j beta_j^2 / 2 after the L1 sum. */
+static double penalty_value(const double* gamma, const double* l2, const double* beta, int64_t p) {
     double total = 0.0;
     for (int64_t j = 0; j < p; ++j) total += gamma[j] * fabs(beta[j]);
+    if (l2)
+        for (int64_t j = 0; j < p; ++j) total += 0.5 * l2[j] * beta[j] * beta[j];
     return total;
+}
+
+/* Elastic-net coordinate rule (extension, not in the reference): the ridge
+ * term adds l2*beta to g' and l2 to g'', then the reference's L1 rule
+ * (optimizer.cpp:51-78) runs on the penalised pair. l2 = 0 is the reference
+ * rule bit for bit (g1 + 0*beta == g1, g2 + 0 == g2). */
+int orc_coordinate_update(double g1, double g2, double beta_j, double gamma_j, double l2_j,
+                          double* step, int* skipped, int* flat) {
+    return orc_l1_coordinate_update(g1 + l2_j * beta_j, g2 + l2_j, beta_j, gamma_j, step, skipped,
+                                    flat);
 }
 
 /* run_ccd + ccd_fit, optimizer.cpp:82-160 */
@@ -568,10 +582,24 @@ int orc_ccd_fit(const orc_design* d, const double* gamma, int max_cycles, double
                 double initial_trust, int64_t chunk, const double* initial_beta,
                 double* beta_out, double* trace_out, int* trace_len, int* cycles,
                 int* converged, double* trust_out, int* n_warnings) {
+    return orc_ccd_fit_prior(d, gamma, NULL, max_cycles, tolerance, initial_trust, chunk,
+                             initial_beta, beta_out, trace_out, trace_len, cycles, converged,
+                             trust_out, n_warnings);
+}
+
+/* The same with an optional L2 prior l2[p] (NULL: none). */
+int orc_ccd_fit_prior(const orc_design* d, const double* gamma, const double* l2, int max_cycles,
+                      double tolerance, double initial_trust, int64_t chunk,
+                      const double* initial_beta, double* beta_out, double* trace_out,
+                      int* trace_len, int* cycles, int* converged, double* trust_out,
+                      int* n_warnings) {
     const int64_t p = d->p, n = d->n;
     for (int64_t j = 0; j < p; ++j) /* PenaltySpec::validate, optimizer.cpp:24-30 */
         if (!isfinite(gamma[j]) || gamma[j] < 0.0)
             return fail(ORC_VALIDATION, "penalty weights must be finite and non-negative");
+    for (int64_t j = 0; l2 && j < p; ++j)
+        if (!isfinite(l2[j]) || l2[j] < 0.0)
+            return fail(ORC_VALIDATION, "L2 prior weights must be finite and non-negative");
     if (max_cycles < 1) return fail(ORC_VALIDATION, "max_cycles must be >= 1");
     if (!(tolerance > 0.0)) return fail(ORC_VALIDATION, "tolerance must be positive");
     if (!(initial_trust > 0.0)) return fail(ORC_VALIDATION, "initial_trust must be positive");
@@ -592,7 +620,7 @@ int orc_ccd_fit(const orc_design* d, const double* gamma, int max_cycles, double
     double ll;
     rc = orc_log_partial_likelihood(d, xb, ex, chunk, &ll);
     if (rc) goto out;
-    double objective = -ll + penalty_value(gamma, beta, p);
+    double objective = -ll + penalty_value(gamma, l2, beta, p);
     trace_out[len++] = objective;
 
     for (int cycle = 1; cycle <= max_cycles; ++cycle) {
@@ -605,7 +633,7 @@ int orc_ccd_fit(const orc_design* d, const double* gamma, int max_cycles, double
             }
             double step;
             int skipped, flat;
-            rc = orc_l1_coordinate_update(g, h, beta[j], gamma[j], &step, &skipped, &flat);
+            rc = orc_coordinate_update(g, h, beta[j], gamma[j], l2 ? l2[j] : 0.0, &step, &skipped, &flat);
             if (rc) goto out;
             double applied;
             rc = orc_apply_trust_region(step, trust[j], &applied, NULL);
@@ -628,7 +656,7 @@ int orc_ccd_fit(const orc_design* d, const double* gamma, int max_cycles, double
         }
         rc = orc_log_partial_likelihood(d, xb, ex, chunk, &ll);
         if (rc) goto out;
-        const double next = -ll + penalty_value(gamma, beta, p);
+        const double next = -ll + penalty_value(gamma, l2, beta, p);
         if (next > objective + 1e-8) {
             rc = fail(ORC_NUMERIC, "monotonicity violated: objective rose from %f to %f", objective,
                       next);

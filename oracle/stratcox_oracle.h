@@ -87,6 +87,17 @@ int orc_ccd_fit(const orc_design* d, const double* gamma, int max_cycles, double
                 double* beta_out, double* trace_out, int* trace_len, int* cycles,
                 int* converged, double* trust_out, int* n_warnings);
 
+/* Extension (not in the reference; BASELINE config 1 "L2 prior"): ridge term
+ * sum l2_j beta_j^2 / 2 added to the objective, g' += l2 beta, g'' += l2 before
+ * the L1 rule. l2 == NULL is orc_ccd_fit. */
+int orc_coordinate_update(double g1, double g2, double beta_j, double gamma_j, double l2_j,
+                          double* step, int* skipped, int* flat);
+int orc_ccd_fit_prior(const orc_design* d, const double* gamma, const double* l2, int max_cycles,
+                      double tolerance, double initial_trust, int64_t chunk,
+                      const double* initial_beta, double* beta_out, double* trace_out,
+                      int* trace_len, int* cycles, int* converged, double* trust_out,
+                      int* n_warnings);
+
 /* resample.cpp:42-55 (every coefficient penalized, as PenaltySpec::shared) */
 int orc_gamma_max(const orc_design* d, int64_t chunk, double* out);
 

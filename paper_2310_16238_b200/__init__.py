@@ -35,6 +35,7 @@ from .stratcox import (  # noqa: F401
     gamma_max,
     gradient_hessian,
     l1_coordinate_update,
+    coordinate_update,
     log_partial_likelihood,
     make_state,
     naive_gradient_hessian,

@@ -74,8 +74,12 @@ SIGNATURES = {
     "scx_apply_trust_region": (C.c_int, [C.c_double, C.c_double, _dp, _dp]),
     "scx_l1_coordinate_update": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, _dp,
                                            _ip, _ip]),
+    "scx_coordinate_update": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double,
+                                        C.c_double, _dp, _ip, _ip]),
     "scx_rule_error": (C.c_char_p, []),
     "scx_ccd_fit": (C.c_int, [_vp, _dp, C.POINTER(FitOptions), _dp, C.POINTER(FitResultC)]),
+    "scx_ccd_fit_prior": (C.c_int, [_vp, _dp, _dp, C.POINTER(FitOptions), _dp,
+                                    C.POINTER(FitResultC)]),
     "scx_gamma_max": (C.c_int, [_vp, _dp, _dp]),
     "scx_timing_enable": (C.c_int, [_vp, C.c_int]),
     "scx_timing_reset": (C.c_int, [_vp]),

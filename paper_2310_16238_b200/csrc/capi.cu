@@ -168,7 +168,7 @@ scx_status cuda_fail(scx_ctx* c, cudaError_t e, const char* where) {
 
 void free_design(scx_ctx* ctx) {
     DesignDev& d = ctx->d;
-    void* ptrs[] = {d.code,   d.D,          d.eta,         d.beta,      d.gamma,
+    void* ptrs[] = {d.code,   d.D,          d.eta,         d.beta,      d.gamma,     d.l2,
                     d.trust,  d.status,     d.slots,       d.partial,   ctx->xdense,
                     ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
                     ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d, d.lasth1,
@@ -665,6 +665,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     CK(dmalloc(&d.eta, d.npad));
     CK(dmalloc(&d.beta, p));
     CK(dmalloc(&d.gamma, p));
+    CK(dmalloc(&d.l2, p));
     CK(dmalloc(&d.trust, p));
     CK(dmalloc(&d.lasth1, d.ntiles1));
     KL(1, launch_last_head(d.lasth1, ctx->offsets_d, k, d.ntiles1, s));
@@ -733,6 +734,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     CK(cudaMemsetAsync(d.eta, 0, d.npad * sizeof(double), s));
     CK(cudaMemsetAsync(d.beta, 0, std::max<int64_t>(p, 1) * sizeof(double), s));
     CK(cudaMemsetAsync(d.gamma, 0, std::max<int64_t>(p, 1) * sizeof(double), s));
+    CK(cudaMemsetAsync(d.l2, 0, std::max<int64_t>(p, 1) * sizeof(double), s));
     CK(cudaMemsetAsync(d.status, 0, d.ntiles * sizeof(unsigned int), s));
     d.rows = ctx->rows_d;
     d.vals = ctx->vals_d;
@@ -1090,6 +1092,18 @@ scx_status scx_apply_trust_region(double proposed, double trust, double* applied
     return s;
 }
 
+scx_status scx_coordinate_update(double g1, double g2, double beta_j, double gamma_j, double l2_j,
+                                 double* step, int* skipped, int* flat) {
+    int sk = 0, fl = 0;
+    const char* m;
+    const scx_status s =
+        rule_status(coordinate_update(g1, g2, beta_j, gamma_j, l2_j, step, &sk, &fl), &m);
+    if (skipped) *skipped = sk;
+    if (flat) *flat = fl;
+    g_rule_msg = m;
+    return s;
+}
+
 scx_status scx_l1_coordinate_update(double g1, double g2, double beta_j, double gamma_j,
                                     double* step, int* skipped, int* flat) {
     int sk = 0, fl = 0;
@@ -1112,7 +1126,7 @@ static scx_status run_cycle_tail(scx_ctx* ctx, bool end_of_cycle, double* ll, do
     // zero columns: gradient (0, 0) -> flat -> applied 0 -> trust halves
     // (optimizer.cpp:103-124); batched at the end of the cycle.
     if (end_of_cycle)
-        KL(1, launch_trust_halve(d.trust, ctx->zero_cols_d, (int64_t)ctx->zero_cols.size(), s));
+        KL(1, launch_zero_cols(d, ctx->zero_cols_d, (int64_t)ctx->zero_cols.size(), s));
     if (ctx->nranks > 1) {
         // log-likelihood and max|eta| are rank-local: gather and reduce in rank order
         tmark(ctx, 2);
@@ -1214,6 +1228,12 @@ static scx_status run_coordinate(scx_ctx* ctx, const ColArgs& col) {
 
 scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options* opt,
                        const double* initial_beta, scx_fit_result* res) {
+    return scx_ccd_fit_prior(ctx, gamma, nullptr, opt, initial_beta, res);
+}
+
+scx_status scx_ccd_fit_prior(scx_ctx* ctx, const double* gamma, const double* l2,
+                             const scx_fit_options* opt, const double* initial_beta,
+                             scx_fit_result* res) {
     if (scx_status s = need_design(ctx)) return s;
     DesignDev& d = ctx->d;
     const int64_t p = d.p;
@@ -1221,6 +1241,9 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
     for (int64_t j = 0; j < p; ++j)
         if (!std::isfinite(gamma[j]) || gamma[j] < 0.0)
             return fail(ctx, SCX_ERR_VALIDATION, "penalty weights must be finite and non-negative");
+    for (int64_t j = 0; l2 && j < p; ++j)
+        if (!std::isfinite(l2[j]) || l2[j] < 0.0)
+            return fail(ctx, SCX_ERR_VALIDATION, "L2 prior weights must be finite and non-negative");
     if (opt->max_cycles < 1) return fail(ctx, SCX_ERR_VALIDATION, "max_cycles must be >= 1");
     if (!(opt->tolerance > 0.0)) return fail(ctx, SCX_ERR_VALIDATION, "tolerance must be positive");
     if (!(opt->initial_trust > 0.0))
@@ -1238,6 +1261,10 @@ scx_status scx_ccd_fit(scx_ctx* ctx, const double* gamma, const scx_fit_options*
     for (auto& v : ctx->rs_stats) v = 0;
     if (p > 0) {
         CK(cudaMemcpyAsync(d.gamma, gamma, p * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (l2)
+            CK(cudaMemcpyAsync(d.l2, l2, p * sizeof(double), cudaMemcpyHostToDevice, s));
+        else
+            CK(cudaMemsetAsync(d.l2, 0, p * sizeof(double), s));
         CK(cudaMemcpyAsync(d.beta, beta0.data(), p * sizeof(double), cudaMemcpyHostToDevice, s));
         k_fill<<<std::max(1, (int)std::min<int64_t>((p + 255) / 256, 1184)), 256, 0, s>>>(
             d.trust, opt->initial_trust, p);

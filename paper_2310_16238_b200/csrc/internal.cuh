@@ -263,6 +263,7 @@ struct DesignDev {
     const int64_t* offsets;   // [k+1]
     double* beta;
     double* gamma;
+    double* l2;               // [p] L2 prior weights (extension; zeros unless a prior is given)
     double* trust;
     // look-back scratch
     unsigned int* status;     // [ntiles]
@@ -306,8 +307,7 @@ cudaError_t launch_refresh(const DesignDev& d, cudaStream_t s);
 cudaError_t launch_naive_gh(const DesignDev& d, const ColArgs& col, double* xdense,
                             double* out2, cudaStream_t s);
 cudaError_t launch_naive_ll(const DesignDev& d, double* out1, cudaStream_t s);
-cudaError_t launch_trust_halve(double* trust, const int32_t* cols, int64_t ncols,
-                               cudaStream_t s);
+cudaError_t launch_zero_cols(const DesignDev& d, const int32_t* cols, int64_t ncols, cudaStream_t s);
 cudaError_t launch_rank_step(const DesignDev& d, const ColArgs& col, const double* parts,
                              int nranks, cudaStream_t s);
 // design preparation

@@ -80,4 +80,19 @@ __host__ __device__ inline int l1_coordinate_update(double g1, double g2, double
     return newton_step(penalized, g2, step, flat);
 }
 
+// Elastic-net rule (extension; not in the reference — BASELINE config 1's
+// "L2 prior"): the ridge term l2_j beta_j^2 / 2 adds l2_j beta_j to g' and l2_j
+// to g'', then the reference's L1 rule runs on the penalised pair. With
+// l2_j = 0 this is l1_coordinate_update bit for bit (g1 + 0*beta == g1).
+__host__ __device__ inline int coordinate_update(double g1, double g2, double beta_j,
+                                                 double gamma_j, double l2_j, double* step,
+                                                 int* skipped, int* flat) {
+#ifdef __CUDA_ARCH__
+    const double pg = __dadd_rn(g1, __dmul_rn(l2_j, beta_j));  // no FMA: the host's rounding
+#else
+    const double pg = g1 + l2_j * beta_j;
+#endif
+    return l1_coordinate_update(pg, g2 + l2_j, beta_j, gamma_j, step, skipped, flat);
+}
+
 }  // namespace scx

@@ -425,11 +425,32 @@ def l1_coordinate_update(g1: float, g2: float, beta_j: float, gamma_j: float) ->
     return ProposedStep(s.value, bool(sk.value), bool(fl.value))
 
 
+def coordinate_update(g1: float, g2: float, beta_j: float, gamma_j: float,
+                      l2_j: float) -> ProposedStep:
+    """Elastic-net rule (extension; no reference counterpart): ridge term
+    l2_j*beta_j^2/2 folded into (g', g''), then l1_coordinate_update."""
+    s = C.c_double(); sk = C.c_int(); fl = C.c_int()
+    _check(_lib().scx_coordinate_update(float(g1), float(g2), float(beta_j), float(gamma_j),
+                                        float(l2_j), C.byref(s), C.byref(sk), C.byref(fl)),
+           rule=True)
+    return ProposedStep(s.value, bool(sk.value), bool(fl.value))
+
+
 @dataclass
 class PenaltySpec:
-    """PenaltySpec (optimizer.hpp:18-28): per-coefficient L1 weight, 0 = unpenalized."""
+    """PenaltySpec (optimizer.hpp:18-28): per-coefficient L1 weight, 0 = unpenalized.
+
+    ``l2`` (extension, not in the reference): optional per-coefficient L2
+    (ridge / Gaussian) prior weight; the objective adds sum l2_j beta_j^2 / 2.
+    BASELINE config 1's "L2 prior" is ``PenaltySpec.ridge(p, lam)``."""
 
     gamma: np.ndarray
+    l2: Optional[np.ndarray] = None
+
+    @staticmethod
+    def ridge(p: int, l2_value: float, gamma_value: float = 0.0) -> "PenaltySpec":
+        return PenaltySpec(np.full(p, float(gamma_value), np.float64),
+                           np.full(p, float(l2_value), np.float64))
 
     @staticmethod
     def none(p: int) -> "PenaltySpec":
@@ -448,6 +469,9 @@ class PenaltySpec:
         total = 0.0
         for gj, bj in zip(self.gamma, beta):
             total += gj * abs(bj)
+        if self.l2 is not None:
+            for lj, bj in zip(self.l2, beta):
+                total += 0.5 * lj * bj * bj
         return total
 
     def validate(self, p: int):
@@ -456,6 +480,12 @@ class PenaltySpec:
         g = np.asarray(self.gamma, np.float64)
         if not np.all(np.isfinite(g)) or np.any(g < 0.0):
             raise ValidationError("penalty weights must be finite and non-negative")
+        if self.l2 is not None:
+            lam = np.asarray(self.l2, np.float64)
+            if lam.shape != (p,):
+                raise ValidationError("L2 prior length does not match covariate count")
+            if not np.all(np.isfinite(lam)) or np.any(lam < 0.0):
+                raise ValidationError("L2 prior weights must be finite and non-negative")
 
 
 @dataclass
@@ -505,8 +535,9 @@ def ccd_fit(dd: DeviceDesign, penalty: PenaltySpec, config: Optional[OptimizerCo
     if dd._state_owner is not None:
         dd._state_owner._snapshot()
         dd._state_owner = None
-    _check(_lib().scx_ccd_fit(dd.handle, ptr(gamma, C.c_double), C.byref(opt),
-                              ptr(ib, C.c_double), C.byref(res)), dd.handle)
+    lam = None if penalty.l2 is None else np.ascontiguousarray(penalty.l2, dtype=np.float64)
+    _check(_lib().scx_ccd_fit_prior(dd.handle, ptr(gamma, C.c_double), ptr(lam, C.c_double),
+                                    C.byref(opt), ptr(ib, C.c_double), C.byref(res)), dd.handle)
     warnings = [f"coordinate {dd.design.covariate_name(int(j))} skipped: step overflow persisted "
                 f"after 10 halvings" for j in wc[:min(res.n_warnings, wcap)]]
     if res.n_warnings > wcap:
