@@ -33,11 +33,15 @@ $(OBJDIR)/cv.o: $(CSRC)/cv.cu $(CSRC)/internal.cuh include/stratcox_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/cv.ptxas.txt || (cat $(OBJDIR)/cv.ptxas.txt; exit 1)
 
+$(OBJDIR)/design_build.o: $(CSRC)/design_build.cu $(CSRC)/internal.cuh include/stratcox_b200.h
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/design_build.ptxas.txt || (cat $(OBJDIR)/design_build.ptxas.txt; exit 1)
+
 $(OBJDIR)/transforms.o: $(CSRC)/transforms.cu $(CSRC)/internal.cuh include/stratcox_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/transforms.ptxas.txt || (cat $(OBJDIR)/transforms.ptxas.txt; exit 1)
 
-$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o $(OBJDIR)/transforms.o
+$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o $(OBJDIR)/transforms.o $(OBJDIR)/design_build.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
 oracle: lib

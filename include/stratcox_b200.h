@@ -79,6 +79,15 @@ scx_status scx_design_info(const scx_ctx* ctx, int64_t* n_rows, int32_t* n_strat
                            int64_t* nnz, int32_t* code_bytes, int64_t* n_tiles,
                            int64_t* n_indicator);
 
+/* The uploaded SortedDesign back on the host (any pointer may be NULL):
+ * stratum_offsets [n_strata+1], event [n], tie_group_end [n], col_ptr [p+1],
+ * row_idx [nnz] (sorted rows), values [nnz] (1.0 for indicator columns).
+ * With scx_build_design this is build_sorted_design (data.cpp:68-147) run on
+ * the device; the C++ drop-in returns it as the reference's SortedDesign. */
+scx_status scx_design_export(scx_ctx* ctx, int64_t* stratum_offsets, uint8_t* event,
+                             int64_t* tie_group_end, int64_t* col_ptr, int64_t* row_idx,
+                             double* values);
+
 /* ---------------------------------------------------------------- state
  * CoefficientState (likelihood.hpp:23-29) lives on the device. */
 /* make_state (likelihood.hpp:33, likelihood.cpp:19-29): beta[p] -> eta, D. */
@@ -205,10 +214,12 @@ typedef struct {
     const double* values;     /* [nnz] or NULL (every value 1.0) */
 } scx_dataset;
 
-/* build_sorted_design (data.cpp:68-147: stable sort by stratum ascending,
- * time descending; CSC re-index; heads; tie-group ends) on the host, then
- * upload (as scx_upload_design). perm_out [n] may be NULL: sorted row s is
- * input row perm_out[s]. */
+/* build_sorted_design (data.cpp:68-147) with validate_invariants
+ * (data.cpp:27-66) ON THE DEVICE: stable LSD radix sorts by (stratum asc,
+ * time desc), heads, tie-group ends and the CSC re-index (a segmented radix
+ * sort per column), then the upload (as scx_upload_design). Same permutation,
+ * same arrays and same validation messages as the reference. perm_out [n]
+ * may be NULL: sorted row s is input row perm_out[s]. */
 scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, int64_t* perm_out);
 
 /* default_gamma_grid (resample.hpp:42, resample.cpp:57-68): `size` values

@@ -81,6 +81,9 @@ SIGNATURES = {
     "scx_ccd_fit_prior": (C.c_int, [_vp, _dp, _dp, C.POINTER(FitOptions), _dp,
                                     C.POINTER(FitResultC)]),
     "scx_gamma_max": (C.c_int, [_vp, _dp, _dp]),
+    "scx_design_export": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_uint8),
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64), _dp]),
     "scx_timing_enable": (C.c_int, [_vp, C.c_int]),
     "scx_timing_reset": (C.c_int, [_vp]),
     "scx_timing_get": (C.c_int, [_vp, C.c_int, _dp, _i64p]),

@@ -171,7 +171,8 @@ void free_design(scx_ctx* ctx) {
     void* ptrs[] = {d.code,   d.D,          d.eta,         d.beta,      d.gamma,     d.l2,
                     d.trust,  d.status,     d.slots,       d.partial,   ctx->xdense,
                     ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
-                    ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d, d.lasth1,
+                    ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d, d.lasth1, d.ref_act,
+                    d.ref_abeg, d.ref_avo, d.ref_ab, d.ref_nact, d.ref_meta,
                     d.chunk_rows, ctx->cols_d, d.rs_u, d.rs_R, d.rs_Q, d.chunk_k, ctx->col1_d};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -532,10 +533,24 @@ const char* scx_last_error(const scx_ctx* ctx) { return ctx ? ctx->err.c_str() :
 
 void* scx_stream(scx_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
+// Sorted arrays already on the device (the device design build,
+// design_build.cu): event and tie ends are read in place; the int32 rows and
+// the compacted values pass to the context; the column classification was
+// done by the builder.
+struct DevSrc {
+    const uint8_t* event_d;
+    const int64_t* tie_d;
+    int32_t* rows32_d;
+    double* vals_d;
+    const std::vector<int64_t>* val_off;
+    int64_t n_ind;
+};
+
 static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_t* offsets,
                                 const uint8_t* event, const int64_t* tie_end, int64_t p,
                                 const int64_t* col_ptr, const int64_t* row64,
-                                const int32_t* row32, const double* values) {
+                                const int32_t* row32, const double* values,
+                                const DevSrc* dev = nullptr) {
     if (!ctx) return SCX_ERR_VALIDATION;
     cudaSetDevice(ctx->device);
     if (n < 1) return fail(ctx, SCX_ERR_VALIDATION, "dataset has no rows");
@@ -561,7 +576,11 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     std::vector<int64_t> val_off(p, -1);
     std::vector<double> compact;
     int64_t n_ind = 0;
-    for (int64_t j = 0; j < p; ++j) {
+    if (dev) {
+        val_off = *dev->val_off;
+        n_ind = dev->n_ind;
+    }
+    for (int64_t j = 0; j < p && !dev; ++j) {
         bool ind = true;
         if (values) {
             for (int64_t t = col_ptr[j]; t < col_ptr[j + 1]; ++t) {
@@ -594,13 +613,18 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     int64_t* tie_d = nullptr;
     uint32_t* w_d = nullptr;
     unsigned int* maxw_d = nullptr;
-    CK(dmalloc(&event_d, n));
-    CK(dmalloc(&tie_d, n));
+    if (dev) {
+        event_d = const_cast<uint8_t*>(dev->event_d);
+        tie_d = const_cast<int64_t*>(dev->tie_d);
+    } else {
+        CK(dmalloc(&event_d, n));
+        CK(dmalloc(&tie_d, n));
+        CK(cudaMemcpyAsync(event_d, event, n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(tie_d, tie_end, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    }
     CK(dmalloc(&w_d, d.npad));
     CK(dmalloc(&maxw_d, 1));
     CK(dmalloc(&ctx->offsets_d, k + 1));
-    CK(cudaMemcpyAsync(event_d, event, n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(tie_d, tie_end, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->offsets_d, offsets, (k + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
                        s));
     CK(cudaMemsetAsync(w_d, 0, d.npad * sizeof(uint32_t), s));
@@ -613,18 +637,29 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     CK(cudaMalloc(&d.code, d.npad * d.code_bytes));
     KL(1, launch_build_codes(d.code, d.code_bytes, n, d.npad, event_d, tie_d, ctx->offsets_d, k, w_d,
                           s));
-    ctx->tie_end_h.assign(tie_end, tie_end + n);
-    ctx->event_h.assign(event, event + n);
+    if (dev) {  // host copies for error-message row mapping
+        ctx->tie_end_h.resize(n);
+        ctx->event_h.resize(n);
+        CK(cudaMemcpyAsync(ctx->tie_end_h.data(), tie_d, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->event_h.data(), event_d, n, cudaMemcpyDeviceToHost, s));
+    } else {
+        ctx->tie_end_h.assign(tie_end, tie_end + n);
+        ctx->event_h.assign(event, event + n);
+    }
 
     // --- CSC
-    CK(dmalloc(&ctx->rows_d, nnz + 16));  // +16: 16-B-aligned bulk copies may overhang
+    if (dev)
+        ctx->rows_d = dev->rows32_d;  // sorted on the device, nnz + 16 entries
+    else
+        CK(dmalloc(&ctx->rows_d, nnz + 16));  // +16: 16-B-aligned bulk copies may overhang
     CK(dmalloc(&ctx->col_beg_d, p + 1));
     CK(dmalloc(&ctx->val_off_d, p));
     CK(cudaMemcpyAsync(ctx->col_beg_d, col_ptr, (p + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
                        s));
     CK(cudaMemcpyAsync(ctx->val_off_d, val_off.data(), p * sizeof(int64_t),
                        cudaMemcpyHostToDevice, s));
-    if (row32) {
+    if (dev) {
+    } else if (row32) {
         CK(cudaMemcpyAsync(ctx->rows_d, row32, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     } else if (nnz > 0) {
         const int64_t chunk = std::min<int64_t>(nnz, (int64_t)1 << 26);
@@ -639,7 +674,10 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         cudaFree(stage);
     }
     if (nnz > 0) k_check_rows<<<1184, 256, 0, s>>>(ctx->rows_d, ctx->col_beg_d, p, nnz, n, d.ctl);
-    CK(dmalloc(&ctx->vals_d, compact.size() + 16));
+    if (dev)
+        ctx->vals_d = dev->vals_d;
+    else
+        CK(dmalloc(&ctx->vals_d, compact.size() + 16));
     if (!compact.empty())
         CK(cudaMemcpyAsync(ctx->vals_d, compact.data(), compact.size() * sizeof(double),
                            cudaMemcpyHostToDevice, s));
@@ -653,9 +691,18 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         CK(cudaMemcpyAsync(stats.data(), stats_d, p * sizeof(ColStats), cudaMemcpyDeviceToHost, s));
     CK(dmalloc(&ctx->tptr_d, p * (d.ntiles1 + 1)));
     if (p > 0) KL(1, launch_tile_ptr(ctx->tptr_d, ctx->rows_d, ctx->col_beg_d, p, d.ntiles1, s));
+    d.ref_ps = (std::max<int64_t>(p, 1) + 31) / 32 * 32;
+    CK(dmalloc(&d.ref_act, d.ref_ps));
+    CK(dmalloc(&d.ref_abeg, d.ref_ps));
+    CK(dmalloc(&d.ref_avo, d.ref_ps));
+    CK(dmalloc(&d.ref_ab, d.ref_ps));
+    CK(dmalloc(&d.ref_nact, 1));
+    CK(dmalloc(&d.ref_meta, d.ref_ps * (d.ntiles1 + 1)));
     CK(cudaStreamSynchronize(s));
-    cudaFree(event_d);
-    cudaFree(tie_d);
+    if (!dev) {
+        cudaFree(event_d);
+        cudaFree(tie_d);
+    }
     cudaFree(w_d);
     cudaFree(maxw_d);
     cudaFree(stats_d);
@@ -750,11 +797,10 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
 
     // co-resident block count for the cooperative kernels
     {
-        int sms = 0, b1 = 0, b2 = 0;
+        int sms = 0, b1 = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k3_apply_ptr(), kThreads, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, refresh_ptr(), kThreads, 0);
-        const int per = std::max(1, std::min(std::min(b1, b2), 2));
+        const int per = std::max(1, std::min(b1, 2));
         d.coop_blocks = sms * per;
     }
 
@@ -801,9 +847,26 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         return st;
     }
     // state at beta = 0 (make_state)
-    KL(1, launch_refresh(d, s));
+    KL(kRefreshLaunches, launch_refresh(d, s));
     return check_device_error(ctx);
 }
+
+}  // extern "C"
+
+// library-internal (C++ linkage): the device design build's hand-off
+scx_status scx_upload_device_design(scx_ctx* ctx, int64_t n, int32_t k, const int64_t* offsets_h,
+                                    const uint8_t* event_d, const int64_t* tie_d, int64_t p,
+                                    const int64_t* col_ptr_h, int32_t* rows32_d, double* vals_d,
+                                    const std::vector<int64_t>& val_off, int64_t n_ind) {
+    DevSrc dev{event_d, tie_d, rows32_d, vals_d, &val_off, n_ind};
+    return upload_common(ctx, n, k, offsets_h, nullptr, nullptr, p, col_ptr_h, nullptr, nullptr,
+                         nullptr, &dev);
+}
+
+cudaStream_t scx_ctx_stream(scx_ctx* ctx) { return ctx->stream; }
+int scx_ctx_device(scx_ctx* ctx) { return ctx->device; }
+
+extern "C" {
 
 scx_status scx_upload_design(scx_ctx* ctx, int64_t n_rows, int32_t n_strata,
                              const int64_t* stratum_offsets, const uint8_t* event,
@@ -837,13 +900,49 @@ scx_status scx_design_info(const scx_ctx* ctx, int64_t* n_rows, int32_t* n_strat
     return SCX_OK;
 }
 
+scx_status scx_design_export(scx_ctx* ctx, int64_t* offsets, uint8_t* event, int64_t* tie_end,
+                             int64_t* col_ptr, int64_t* row_idx, double* values) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    const DesignDev& d = ctx->d;
+    cudaStream_t s = ctx->stream;
+    const int64_t n = d.n, p = d.p, nnz = ctx->nnz;
+    if (offsets)
+        CK(cudaMemcpyAsync(offsets, ctx->offsets_d, (d.k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (event) std::memcpy(event, ctx->event_h.data(), n);
+    if (tie_end) std::memcpy(tie_end, ctx->tie_end_h.data(), n * sizeof(int64_t));
+    std::vector<int64_t> cp(p + 1, 0);
+    for (int64_t j = 0; j < p; ++j) cp[j + 1] = cp[j] + ctx->cols[j].nnz;
+    if (col_ptr) std::memcpy(col_ptr, cp.data(), (p + 1) * sizeof(int64_t));
+    if (row_idx && nnz > 0) {
+        std::vector<int32_t> r32(nnz);
+        CK(cudaMemcpyAsync(r32.data(), ctx->rows_d, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int64_t t = 0; t < nnz; ++t) row_idx[t] = r32[t];
+    }
+    if (values) {
+        for (int64_t j = 0; j < p; ++j) {
+            const ColArgs& c = ctx->cols[j];
+            if (c.nnz == 0) continue;
+            if (c.indicator) {
+                std::fill(values + cp[j], values + cp[j + 1], 1.0);
+            } else {
+                CK(cudaMemcpyAsync(values + cp[j], ctx->vals_d + c.val_off, c.nnz * sizeof(double),
+                                   cudaMemcpyDeviceToHost, s));
+            }
+        }
+    }
+    CK(cudaStreamSynchronize(s));
+    return SCX_OK;
+}
+
 // ---------------------------------------------------------------- state
 scx_status scx_make_state(scx_ctx* ctx, const double* beta) {
     if (scx_status s = need_design(ctx)) return s;
     cudaSetDevice(ctx->device);
     DesignDev& d = ctx->d;
     if (d.p > 0) CK(cudaMemcpyAsync(d.beta, beta, d.p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    KL(1, launch_refresh(d, ctx->stream));
+    KL(kRefreshLaunches, launch_refresh(d, ctx->stream));
     return check_device_error(ctx);
 }
 
@@ -886,7 +985,7 @@ scx_status scx_get_state(scx_ctx* ctx, double* beta, double* xbeta, double* exp_
 scx_status scx_refresh_xbeta(scx_ctx* ctx) {
     if (scx_status s = need_design(ctx)) return s;
     cudaSetDevice(ctx->device);
-    KL(1, launch_refresh(ctx->d, ctx->stream));
+    KL(kRefreshLaunches, launch_refresh(ctx->d, ctx->stream));
     return check_device_error(ctx);
 }
 
@@ -1184,7 +1283,7 @@ static scx_status fused_cycle(scx_ctx* ctx, const ColArgs* cols, int32_t n, bool
     if (resumed) *resumed = r;
     if (r > 0) {
         // 256 accepted updates: refresh eta/D from beta, then resume
-        KL(2, launch_refresh(d, s));
+        KL(kRefreshLaunches, launch_refresh(d, s));
         if (scx_status st = check_device_error(ctx)) return st;
     }
     return SCX_OK;
@@ -1281,7 +1380,7 @@ scx_status scx_ccd_fit_prior(scx_ctx* ctx, const double* gamma, const double* l2
         CK(cudaMemcpyAsync(&c->hmax, &izero, sizeof izero, cudaMemcpyHostToDevice, s));
     }
     // make_state (likelihood.cpp:19-29)
-    KL(1, launch_refresh(d, s));
+    KL(kRefreshLaunches, launch_refresh(d, s));
     if (scx_status st = check_device_error(ctx)) return st;
 
     double ll, pen, max_step;
@@ -1314,7 +1413,7 @@ scx_status scx_ccd_fit_prior(scx_ctx* ctx, const double* gamma, const double* l2
                         const int why = ctx->ctl_h->rs_reason;
                         if (why == kRsDone) break;
                         if (why == kRsRefresh) {
-                            KL(2, launch_refresh(d, s));
+                            KL(kRefreshLaunches, launch_refresh(d, s));
                             if (scx_status st = check_device_error(ctx)) return st;
                         } else if (why == kRsBound) {
                             ctx->rs_stats[2] += 1;

@@ -303,19 +303,8 @@ std::string fmt_gamma(double g) { return std::to_string(g); }  // std::to_string
 
 extern "C" {
 
-scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, int64_t* perm_out) {
-    if (!ctx || !data) return SCX_ERR_VALIDATION;
-    try {
-        const Data d = copy_in(data);
-        const Sorted s = build_sorted(d);
-        upload_sorted(ctx, s, d.p());
-        if (perm_out) std::memcpy(perm_out, s.perm.data(), s.perm.size() * sizeof(int64_t));
-        return SCX_OK;
-    } catch (const ScxError& e) {
-        scx_note_error(ctx, e.what());
-        return e.status;
-    }
-}
+// scx_build_design (the device build of build_sorted_design) is in
+// design_build.cu; build_sorted above prepares the CV folds' designs.
 
 scx_status scx_default_gamma_grid(double gamma_max, int64_t size, double* out) {
     if (size < 1) return SCX_ERR_VALIDATION;  // "gamma grid size must be >= 1"

@@ -1,0 +1,768 @@
+// Device build of the SortedDesign: build_sorted_design,
+// proj/src/data.cpp:68-147, with validate_invariants (data.cpp:27-66) — on the
+// GPU instead of the host.
+//
+//   validation   row checks (time, event, stratum label), empty strata, column
+//                checks (strictly increasing rows, range, finite values), each
+//                reduced to the FIRST failing (row | entry, check) with an
+//                atomicMin on index*4 + check, so the message is the one the
+//                reference's serial loops throw first.
+//   row order    the reference's std::stable_sort by (stratum asc, time desc)
+//                as two stable LSD radix sorts: by ~bits(time) (non-negative
+//                doubles order like their bit patterns; -0.0 is folded onto
+//                +0.0, which compares equal to it), then by stratum label.
+//                Stable + LSD = the same permutation, bit for bit.
+//   CSC          rows re-indexed through the inverse permutation and sorted
+//                inside each column by a segmented LSD radix sort (tiles never
+//                straddle a column), values following their rows.
+//   heads, tie ends, offsets: a flag pass and a reverse min-scan; offsets from
+//                the per-stratum counts of the validation pass.
+//
+// The radix passes: 8-bit digits, 8192-entry tiles (512 threads x 16), a per-
+// tile digit histogram, a scan over (segment, digit, tile), and a stable
+// scatter whose in-tile ranks come from __match_any_sync over warp rows and
+// per-warp digit counters (entries keep their order inside a digit, which is
+// what makes the LSD sort stable). Digits constant over all keys are skipped.
+// No CUB / Thrust.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/stratcox_b200.h"
+#include "internal.cuh"
+
+namespace scx {
+
+constexpr int kRxThreads = 512;
+constexpr int kRxItems = 16;
+constexpr int kRxWarps = kRxThreads / 32;
+constexpr int64_t kRxTile = (int64_t)kRxThreads * kRxItems;  // 8192 entries
+constexpr unsigned long long kNoErr = 0xffffffffffffffffULL;
+
+struct BuildErr {                 // device error words (first failure by index)
+    unsigned long long row_err;   // row * 4 + check (0 time, 1 event, 2 label)
+    unsigned long long ent_err;   // entry * 4 + check (0 order, 1 range, 2 value)
+    int kmax;                     // max stratum label
+    int pad;
+    unsigned long long t_or, t_and;  // varying bits of the time keys
+    unsigned long long k_or, k_and;  // ... of the stratum keys
+    unsigned long long r_or, r_and;  // ... of the re-indexed rows
+};
+
+__device__ __forceinline__ uint64_t time_key(double t) {
+    uint64_t b = (uint64_t)__double_as_longlong(t);
+    if (b == 0x8000000000000000ULL) b = 0;  // -0.0 == +0.0 in the reference's comparator
+    return ~b;                              // descending time = ascending key
+}
+
+// max label; row checks; time keys + identity values; per-stratum counts
+// (labels 1..kcap only: with kmax > n some stratum is empty anyway)
+__global__ void k_b_kmax(const int32_t* stratum, int64_t n, BuildErr* be) {
+    int m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, stratum[i]);
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&be->kmax, m);
+}
+
+__global__ void k_b_rows(const double* time, const uint8_t* event, const int32_t* stratum, int64_t n,
+                         int kmax, int kcap, BuildErr* be, unsigned int* counts, uint64_t* tkey,
+                         uint32_t* idx) {
+    unsigned long long err = kNoErr, o = 0, a = ~0ULL;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double t = time[i];
+        const int32_t s = stratum[i];
+        unsigned long long e = kNoErr;
+        if (!isfinite(t) || t < 0.0)
+            e = (unsigned long long)i * 4 + 0;
+        else if (event[i] > 1)
+            e = (unsigned long long)i * 4 + 1;
+        else if (s < 1 || s > kmax)
+            e = (unsigned long long)i * 4 + 2;
+        err = min(err, e);
+        const bool cnt_it = e == kNoErr && s <= kcap;
+        const unsigned act = __activemask();
+        const unsigned cm = __ballot_sync(act, cnt_it);
+        if (cnt_it) {  // warp-aggregated per-stratum counts
+            const unsigned peers = __match_any_sync(cm, s);
+            if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + (s - 1), __popc(peers));
+        }
+        const uint64_t k = time_key(t);
+        tkey[i] = k;
+        idx[i] = (uint32_t)i;
+        o |= k;
+        a &= k;
+    }
+    for (int q = 16; q; q >>= 1) {
+        err = min(err, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)err, q));
+        o |= (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)o, q);
+        a &= (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)a, q);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (err != kNoErr) atomicMin(&be->row_err, err);
+        atomicOr(&be->t_or, o);
+        atomicAnd(&be->t_and, a);
+    }
+}
+
+// ---------------------------------------------------------------- radix sort
+// Tile map: tile i covers entries [tb[i], tb[i+1]) of segment tseg[i];
+// segment g owns tiles [st0[g], st0[g+1]) and starts at entry sbeg[g].
+struct TileMap {
+    int64_t* tb = nullptr;
+    int32_t* tseg = nullptr;
+    int64_t* st0 = nullptr;
+    int64_t* sbeg = nullptr;
+    int64_t ntiles = 0, nseg = 0;
+};
+
+template <typename K>
+__global__ void __launch_bounds__(kRxThreads) k_rx_hist(const K* keys, const int64_t* tb,
+                                                      int64_t ntiles, int shift, uint32_t* hist) {
+    __shared__ uint32_t h[256];
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (threadIdx.x < 256) h[threadIdx.x] = 0;
+        __syncthreads();
+        const int64_t b = tb[tile], e = tb[tile + 1];
+        for (int64_t i = b + threadIdx.x; i < e; i += kRxThreads)
+            atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 0xffu], 1u);
+        __syncthreads();
+        if (threadIdx.x < 256) hist[tile * 256 + threadIdx.x] = h[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+// (segment, digit) per thread: exclusive prefix over the segment's tiles (in
+// place) and the segment's digit total
+__global__ void k_rx_scan_tiles(uint32_t* hist, const int64_t* st0, int64_t nseg, uint32_t* segtot) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nseg * 256) return;
+    const int64_t seg = g >> 8;
+    const int d = (int)(g & 255);
+    uint32_t run = 0;
+    int64_t t = st0[seg];
+    const int64_t t1 = st0[seg + 1];
+    for (; t + 8 <= t1; t += 8) {
+        uint32_t c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = hist[(t + u) * 256 + d];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            hist[(t + u) * 256 + d] = run;
+            run += c[u];
+        }
+    }
+    for (; t < t1; ++t) {
+        const uint32_t c = hist[t * 256 + d];
+        hist[t * 256 + d] = run;
+        run += c;
+    }
+    segtot[g] = run;
+}
+
+// one warp per segment: exclusive prefix of the 256 digit totals
+__global__ void k_rx_scan_digits(uint32_t* segtot, int64_t nseg) {
+    const int64_t seg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (seg >= nseg) return;
+    uint32_t* t = segtot + seg * 256;
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        v[u] = t[lane * 8 + u];
+        sum += v[u];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += x;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        t[lane * 8 + u] = run;
+        run += v[u];
+    }
+}
+
+// stable scatter of one tile: warp w holds entries [w*512, w*512+512) of the
+// tile, row r of the warp = 32 consecutive entries
+template <typename K, bool VAL>
+__global__ void __launch_bounds__(kRxThreads) k_rx_scatter(const K* kin, const uint32_t* vin, K* kout,
+                                                         uint32_t* vout, const int64_t* tb,
+                                                         const int32_t* tseg, const int64_t* sbeg,
+                                                         const uint32_t* hist, const uint32_t* segbase,
+                                                         int64_t ntiles, int shift) {
+    __shared__ uint16_t wc[kRxWarps][256];
+    __shared__ int64_t tofs[256];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int q = threadIdx.x; q < kRxWarps * 256; q += kRxThreads) (&wc[0][0])[q] = 0;
+        __syncthreads();
+        const int64_t b = tb[tile], e = tb[tile + 1];
+        const int32_t seg = tseg[tile];
+        K k[kRxItems];
+        uint32_t v[kRxItems];
+        uint32_t dg[kRxItems];
+        uint16_t loc[kRxItems];
+#pragma unroll
+        for (int r = 0; r < kRxItems; ++r) {
+            const int64_t i = b + w * (32 * kRxItems) + r * 32 + lane;
+            if (i < e) {
+                k[r] = kin[i];
+                if constexpr (VAL) v[r] = vin[i];
+                dg[r] = (uint32_t)(k[r] >> shift) & 0xffu;
+            } else {
+                dg[r] = 256;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kRxItems; ++r) {
+            const bool ok = dg[r] < 256;
+            const unsigned act = __ballot_sync(0xffffffffu, ok);
+            unsigned peers = 0;
+            uint16_t base = 0;
+            if (ok) {
+                peers = __match_any_sync(act, dg[r]);
+                base = wc[w][dg[r]];
+                loc[r] = (uint16_t)(base + __popc(peers & ((1u << lane) - 1u)));
+            }
+            __syncwarp();
+            if (ok && lane == __ffs(peers) - 1) wc[w][dg[r]] = (uint16_t)(base + __popc(peers));
+            __syncwarp();
+        }
+        __syncthreads();
+        if (threadIdx.x < 256) {
+            const int d = threadIdx.x;
+            uint16_t run = 0;
+            for (int q = 0; q < kRxWarps; ++q) {
+                const uint16_t c = wc[q][d];
+                wc[q][d] = run;
+                run = (uint16_t)(run + c);
+            }
+            tofs[d] = sbeg[seg] + (int64_t)segbase[(int64_t)seg * 256 + d] + hist[tile * 256 + d];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kRxItems; ++r) {
+            if (dg[r] < 256) {
+                const int64_t pos = tofs[dg[r]] + wc[w][dg[r]] + loc[r];
+                kout[pos] = k[r];
+                if constexpr (VAL) vout[pos] = v[r];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+static int grid_sms(int64_t work) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)sms * 8));
+}
+
+// LSD passes over the digits of `varying`; keys/vals ping-pong (the result is
+// left in keys/vals). Stable in every pass.
+template <typename K>
+static cudaError_t radix_sort(K*& keys, K*& kalt, uint32_t*& vals, uint32_t*& valt, bool has_val,
+                              const TileMap& tm, uint64_t varying, uint32_t* hist,
+                              uint32_t* segtot, cudaStream_t s) {
+    if (tm.ntiles == 0) return cudaSuccess;
+    for (int shift = 0; shift < (int)(8 * sizeof(K)); shift += 8) {
+        if (((varying >> shift) & 0xffu) == 0) continue;
+        const int g = grid_sms(tm.ntiles);
+        k_rx_hist<K><<<g, kRxThreads, 0, s>>>(keys, tm.tb, tm.ntiles, shift, hist);
+        const int64_t nt = tm.nseg * 256;
+        k_rx_scan_tiles<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(hist, tm.st0, tm.nseg, segtot);
+        k_rx_scan_digits<<<(unsigned)((tm.nseg * 32 + 255) / 256), 256, 0, s>>>(segtot, tm.nseg);
+        if (has_val)
+            k_rx_scatter<K, true><<<g, kRxThreads, 0, s>>>(keys, vals, kalt, valt, tm.tb, tm.tseg,
+                                                          tm.sbeg, hist, segtot, tm.ntiles, shift);
+        else
+            k_rx_scatter<K, false><<<g, kRxThreads, 0, s>>>(keys, vals, kalt, valt, tm.tb, tm.tseg,
+                                                           tm.sbeg, hist, segtot, tm.ntiles, shift);
+        std::swap(keys, kalt);
+        if (has_val) std::swap(vals, valt);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- sorted rows
+// stratum key of sorted position s under the current permutation
+__global__ void k_b_gather_str(const uint32_t* perm, const int32_t* stratum, int64_t n, uint32_t* key,
+                               BuildErr* be) {
+    unsigned long long o = 0, a = ~0ULL;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = (uint32_t)stratum[perm[i]];
+        key[i] = k;
+        o |= k;
+        a &= k;
+    }
+    for (int q = 16; q; q >>= 1) {
+        o |= (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)o, q);
+        a &= (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)a, q);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(&be->k_or, o);
+        atomicAnd(&be->k_and, a);
+    }
+}
+
+// inverse permutation, sorted event / time / stratum, tie-group-end flags
+__global__ void k_b_sorted(const uint32_t* perm, const double* time, const uint8_t* event,
+                           const int32_t* stratum, int64_t n, uint32_t* inv, uint8_t* ev_s,
+                           int64_t* perm_out, double* time_s, int32_t* str_s) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = perm[s];
+        inv[r] = (uint32_t)s;
+        ev_s[s] = event[r];
+        time_s[s] = time[r];
+        str_s[s] = stratum[r];
+        perm_out[s] = r;
+    }
+}
+
+// tie_group_end (data.cpp:135-145): the last row of the run of equal
+// (stratum, time) that holds s. Reverse min-scan of the run ends, 1024 rows
+// per block; the carry across blocks comes from k_b_tie_blocks.
+constexpr int kTieBlock = 1024;
+__device__ __forceinline__ bool run_end(const double* t, const int32_t* k, int64_t n, int64_t s) {
+    return s == n - 1 || k[s + 1] != k[s] || t[s + 1] != t[s];
+}
+__global__ void k_b_tie_blocks(const double* t, const int32_t* k, int64_t n, int64_t* bmin) {
+    __shared__ int64_t red[32];
+    const int64_t b0 = (int64_t)blockIdx.x * kTieBlock;
+    const int64_t s = b0 + threadIdx.x;
+    int64_t m = INT64_MAX;
+    if (s < n && run_end(t, k, n, s)) m = s;
+    for (int o = 16; o; o >>= 1) m = min(m, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = red[threadIdx.x];
+        for (int o = 16; o; o >>= 1) m = min(m, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)m, o));
+        if (threadIdx.x == 0) bmin[blockIdx.x] = m;
+    }
+}
+// carry[b] = min over blocks > b (one block of 1024 threads, serial chunks)
+__global__ void k_b_tie_carry(const int64_t* bmin, int64_t nb, int64_t* carry) {
+    __shared__ int64_t part[1024];
+    const int64_t per = (nb + 1023) / 1024;
+    const int64_t a = threadIdx.x * per, e = min(nb, a + per);
+    int64_t m = INT64_MAX;
+    for (int64_t b = a; b < e; ++b) m = min(m, bmin[b]);
+    part[threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // suffix minima of the parts, in place
+        int64_t run = INT64_MAX;
+        for (int q = 1023; q >= 0; --q) {
+            const int64_t v = part[q];
+            part[q] = run;  // exclusive: parts after q
+            run = min(run, v);
+        }
+    }
+    __syncthreads();
+    int64_t run = part[threadIdx.x];
+    for (int64_t b = e - 1; b >= a; --b) {
+        carry[b] = run;
+        run = min(run, bmin[b]);
+    }
+}
+__global__ void k_b_tie_apply(const double* t, const int32_t* k, int64_t n, const int64_t* carry,
+                              int64_t* tie_end) {
+    __shared__ int64_t wmin[32];
+    const int64_t s = (int64_t)blockIdx.x * kTieBlock + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t m = (s < n && run_end(t, k, n, s)) ? s : INT64_MAX;
+    // inclusive suffix min inside the warp (lanes above)
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t x = (int64_t)__shfl_down_sync(0xffffffffu, (long long)m, o);
+        if (lane + o < 32) m = min(m, x);
+    }
+    if (lane == 0) wmin[w] = m;
+    __syncthreads();
+    int64_t c = carry[blockIdx.x];
+    for (int q = w + 1; q < 32; ++q) c = min(c, wmin[q]);
+    if (s < n) tie_end[s] = min(m, c);
+}
+
+// ---------------------------------------------------------------- columns
+// H2D-staged int64 rows of whole tiles: column checks (data.cpp:55-64 order),
+// narrowing, re-index through the inverse permutation, value-index payload.
+__global__ void k_b_cols(const int64_t* rows64, int64_t chunk0, const int64_t* tb, int64_t t0,
+                         int64_t t1, const int32_t* tseg, const int64_t* col_ptr, int64_t n,
+                         const uint32_t* inv, uint32_t* key, uint32_t* vidx, int64_t prev_chunk_last,
+                         BuildErr* be) {
+    unsigned long long err = kNoErr, o = 0, a = ~0ULL;
+    for (int64_t tile = t0 + blockIdx.x; tile < t1; tile += gridDim.x) {
+        const int64_t b = tb[tile], e = tb[tile + 1];
+        const int64_t cb = col_ptr[tseg[tile]];
+        for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+            const int64_t r = rows64[i - chunk0];
+            const int64_t prev = i == cb ? -1 : (i > chunk0 ? rows64[i - 1 - chunk0] : prev_chunk_last);
+            uint32_t k = 0;
+            if (r <= prev)
+                err = min(err, (unsigned long long)i * 4 + 0);
+            else if (r < 0 || r >= n)
+                err = min(err, (unsigned long long)i * 4 + 1);
+            else
+                k = inv[r];
+            key[i] = k;
+            if (vidx) vidx[i] = (uint32_t)(i - cb);
+            o |= k;
+            a &= k;
+        }
+    }
+    for (int q = 16; q; q >>= 1) {
+        err = min(err, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)err, q));
+        o |= (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)o, q);
+        a &= (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)a, q);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (err != kNoErr) atomicMin(&be->ent_err, err);
+        atomicOr(&be->r_or, o);
+        atomicAnd(&be->r_and, a);
+    }
+}
+
+// value checks (finite) and the per-column "not all 1.0" flag
+__global__ void k_b_vals(const double* vals, const int64_t* tb, int64_t ntiles, const int32_t* tseg,
+                         uint32_t* nonunit, BuildErr* be) {
+    unsigned long long err = kNoErr;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t b = tb[tile], e = tb[tile + 1];
+        bool nu = false;
+        for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+            const double v = vals[i];
+            if (!isfinite(v)) err = min(err, (unsigned long long)i * 4 + 2);
+            nu |= v != 1.0;
+        }
+        if (__syncthreads_or(nu) && threadIdx.x == 0) nonunit[tseg[tile]] = 1;
+    }
+    for (int q = 16; q; q >>= 1)
+        err = min(err, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)err, q));
+    if ((threadIdx.x & 31) == 0 && err != kNoErr) atomicMin(&be->ent_err, err);
+}
+
+// compacted values of the value columns, following their sorted rows
+__global__ void k_b_vals_out(const uint32_t* vidx, const double* vals, const int64_t* tb,
+                             int64_t ntiles, const int32_t* tseg, const int64_t* col_ptr,
+                             const int64_t* val_off, double* vals_out) {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t b = tb[tile], e = tb[tile + 1];
+        const int32_t j = tseg[tile];
+        const int64_t cb = col_ptr[j], vo = val_off[j];
+        if (vo < 0) continue;
+        for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x)
+            vals_out[vo + (i - cb)] = vals[cb + vidx[i]];
+    }
+}
+
+}  // namespace scx
+
+// ---------------------------------------------------------------- host driver
+using namespace scx;
+
+namespace {
+
+struct DevBuf {
+    std::vector<void*> ptrs;
+    template <typename T>
+    cudaError_t alloc(T** p, size_t count) {
+        cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+        if (e == cudaSuccess) ptrs.push_back(*p);
+        return e;
+    }
+    void release(void* p) {
+        auto it = std::find(ptrs.begin(), ptrs.end(), p);
+        if (it != ptrs.end()) ptrs.erase(it);
+    }
+    ~DevBuf() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+};
+
+// tiles of <= kRxTile entries that never cross a segment boundary
+void make_tiles(const std::vector<int64_t>& seg_ptr, std::vector<int64_t>& tb,
+                std::vector<int32_t>& tseg, std::vector<int64_t>& st0) {
+    const int64_t nseg = (int64_t)seg_ptr.size() - 1;
+    tb.clear();
+    tseg.clear();
+    st0.assign(nseg + 1, 0);
+    for (int64_t g = 0; g < nseg; ++g) {
+        st0[g] = (int64_t)tseg.size();
+        for (int64_t b = seg_ptr[g]; b < seg_ptr[g + 1]; b += kRxTile) {
+            tb.push_back(b);
+            tseg.push_back((int32_t)g);
+        }
+    }
+    st0[nseg] = (int64_t)tseg.size();
+    tb.push_back(seg_ptr[nseg]);
+}
+
+}  // namespace
+
+// Implemented in capi.cu: upload of a design whose sorted arrays are already
+// on the device (ownership of rows32_d / vals_d passes to the context).
+scx_status scx_upload_device_design(scx_ctx* ctx, int64_t n, int32_t k, const int64_t* offsets_h,
+                                    const uint8_t* event_d, const int64_t* tie_d, int64_t p,
+                                    const int64_t* col_ptr_h, int32_t* rows32_d, double* vals_d,
+                                    const std::vector<int64_t>& val_off, int64_t n_ind);
+void scx_note_error(scx_ctx* ctx, const char* msg);
+cudaStream_t scx_ctx_stream(scx_ctx* ctx);
+int scx_ctx_device(scx_ctx* ctx);
+
+#define BK(expr)                                                                   \
+    do {                                                                           \
+        cudaError_t e_ = (expr);                                                   \
+        if (e_ != cudaSuccess) {                                                   \
+            scx_note_error(ctx, (std::string("CUDA error in design build: ") +     \
+                                 cudaGetErrorString(e_)).c_str());                 \
+            return SCX_ERR_CUDA;                                                   \
+        }                                                                          \
+    } while (0)
+
+static scx_status vfail(scx_ctx* ctx, const std::string& m) {
+    scx_note_error(ctx, m.c_str());
+    return SCX_ERR_VALIDATION;
+}
+
+extern "C" scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, int64_t* perm_out) {
+    if (!ctx || !data) return SCX_ERR_VALIDATION;
+    cudaSetDevice(scx_ctx_device(ctx));
+    cudaStream_t s = scx_ctx_stream(ctx);
+    const int64_t n = data->n_rows, p = data->n_covariates;
+    if (n == 0) return vfail(ctx, "dataset has no rows");
+    if (n < 0 || p < 0) return vfail(ctx, "negative dataset size");
+    if (n > (int64_t)0x7fffffff - kTileRows)
+        return vfail(ctx, "row count exceeds the int32 row-index range");
+    const int64_t* col_ptr = data->col_ptr;
+    if (col_ptr[0] != 0) return vfail(ctx, "col_ptr[0] must be 0");
+    for (int64_t j = 0; j < p; ++j)
+        if (col_ptr[j + 1] < col_ptr[j]) return vfail(ctx, "col_ptr must be non-decreasing");
+    const int64_t nnz = col_ptr[p];
+    DevBuf B;
+
+    // ---- rows: upload, label range, row checks, time keys
+    double* time_d;
+    uint8_t* event_d;
+    int32_t* str_d;
+    BuildErr* be;
+    BK(B.alloc(&time_d, n));
+    BK(B.alloc(&event_d, n));
+    BK(B.alloc(&str_d, n));
+    BK(B.alloc(&be, 1));
+    BK(cudaMemcpyAsync(time_d, data->time, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(event_d, data->event, n, cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(str_d, data->stratum, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    {
+        BuildErr init;
+        std::memset(&init, 0, sizeof init);
+        init.row_err = init.ent_err = kNoErr;
+        init.t_and = init.k_and = init.r_and = ~0ULL;
+        BK(cudaMemcpyAsync(be, &init, sizeof init, cudaMemcpyHostToDevice, s));
+    }
+    const int gr = grid_sms((n + 255) / 256);
+    k_b_kmax<<<gr, 256, 0, s>>>(str_d, n, be);
+    BuildErr h;
+    BK(cudaMemcpyAsync(&h, be, sizeof h, cudaMemcpyDeviceToHost, s));
+    BK(cudaStreamSynchronize(s));
+    const int kmax = h.kmax;
+    if (kmax < 1) return vfail(ctx, "dataset has no strata");  // data.cpp:32
+    const int kcap = (int)std::min<int64_t>(kmax, n + 1);
+    unsigned int* cnt_d;
+    uint64_t *tkey, *tkey2;
+    uint32_t *perm, *perm2;
+    BK(B.alloc(&cnt_d, kcap));
+    BK(B.alloc(&tkey, n));
+    BK(B.alloc(&tkey2, n));
+    BK(B.alloc(&perm, n));
+    BK(B.alloc(&perm2, n));
+    BK(cudaMemsetAsync(cnt_d, 0, kcap * sizeof(unsigned int), s));
+    k_b_rows<<<gr, 256, 0, s>>>(time_d, event_d, str_d, n, kmax, kcap, be, cnt_d, tkey, perm);
+    std::vector<unsigned int> cnt(kcap);
+    BK(cudaMemcpyAsync(&h, be, sizeof h, cudaMemcpyDeviceToHost, s));
+    BK(cudaMemcpyAsync(cnt.data(), cnt_d, kcap * sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+    BK(cudaStreamSynchronize(s));
+    if (h.row_err != kNoErr) {  // data.cpp:35-44
+        const int64_t i = (int64_t)(h.row_err / 4);
+        const int c = (int)(h.row_err % 4);
+        const char* what = c == 0 ? "negative or non-finite time at row "
+                           : c == 1 ? "event indicator must be 0 or 1 at row "
+                                    : "stratum label out of range at row ";
+        return vfail(ctx, what + std::to_string(i));
+    }
+    for (int q = 1; q <= kmax; ++q)  // data.cpp:46-49 (some q <= n + 1 is empty when kmax > n)
+        if (q > kcap || cnt[q - 1] == 0)
+            return vfail(ctx, "stratum " + std::to_string(q) + " has zero rows");
+    const int32_t K = kmax;
+    std::vector<int64_t> offsets(K + 1, 0);
+    for (int q = 0; q < K; ++q) offsets[q + 1] = offsets[q] + cnt[q];
+
+    // ---- row permutation: stable by ~time, then stable by stratum
+    TileMap rows_tm;
+    std::vector<int64_t> tb_h, st0_h;
+    std::vector<int32_t> tseg_h;
+    make_tiles({0, n}, tb_h, tseg_h, st0_h);
+    const int64_t ntr = (int64_t)tseg_h.size();
+    int64_t sbeg0 = 0;
+    uint32_t *hist, *segtot;
+    int64_t max_tiles = ntr;
+    // column tiles (for the hist/segtot scratch size)
+    std::vector<int64_t> ctb, cst0;
+    std::vector<int32_t> ctseg;
+    {
+        std::vector<int64_t> sp(col_ptr, col_ptr + p + 1);
+        make_tiles(sp, ctb, ctseg, cst0);
+        max_tiles = std::max<int64_t>(max_tiles, (int64_t)ctseg.size());
+    }
+    BK(B.alloc(&hist, max_tiles * 256));
+    BK(B.alloc(&segtot, std::max<int64_t>(1, p) * 256));
+    BK(B.alloc(&rows_tm.tb, ntr + 1));
+    BK(B.alloc(&rows_tm.tseg, ntr));
+    BK(B.alloc(&rows_tm.st0, 2));
+    BK(B.alloc(&rows_tm.sbeg, 1));
+    BK(cudaMemcpyAsync(rows_tm.tb, tb_h.data(), (ntr + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(rows_tm.tseg, tseg_h.data(), ntr * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(rows_tm.st0, st0_h.data(), 2 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(rows_tm.sbeg, &sbeg0, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    rows_tm.ntiles = ntr;
+    rows_tm.nseg = 1;
+    BK(radix_sort<uint64_t>(tkey, tkey2, perm, perm2, true, rows_tm, h.t_or ^ h.t_and, hist, segtot, s));
+    uint32_t *skey, *skey2;
+    BK(B.alloc(&skey, n));
+    BK(B.alloc(&skey2, n));
+    k_b_gather_str<<<gr, 256, 0, s>>>(perm, str_d, n, skey, be);
+    BK(cudaMemcpyAsync(&h, be, sizeof h, cudaMemcpyDeviceToHost, s));
+    BK(cudaStreamSynchronize(s));
+    BK(radix_sort<uint32_t>(skey, skey2, perm, perm2, true, rows_tm, h.k_or ^ h.k_and, hist, segtot, s));
+
+    // ---- sorted row arrays, tie ends
+    uint32_t* inv;
+    uint8_t* ev_s;
+    int64_t* perm64;
+    double* time_s;
+    int32_t* str_s;
+    int64_t* tie_d;
+    BK(B.alloc(&inv, n));
+    BK(B.alloc(&ev_s, n));
+    BK(B.alloc(&perm64, n));
+    BK(B.alloc(&time_s, n));
+    BK(B.alloc(&str_s, n));
+    BK(B.alloc(&tie_d, n));
+    k_b_sorted<<<gr, 256, 0, s>>>(perm, time_d, event_d, str_d, n, inv, ev_s, perm64, time_s, str_s);
+    const int64_t nb = (n + kTieBlock - 1) / kTieBlock;
+    int64_t *bmin, *carry;
+    BK(B.alloc(&bmin, nb));
+    BK(B.alloc(&carry, nb));
+    k_b_tie_blocks<<<(unsigned)nb, kTieBlock, 0, s>>>(time_s, str_s, n, bmin);
+    k_b_tie_carry<<<1, 1024, 0, s>>>(bmin, nb, carry);
+    k_b_tie_apply<<<(unsigned)nb, kTieBlock, 0, s>>>(time_s, str_s, n, carry, tie_d);
+    if (perm_out)
+        BK(cudaMemcpyAsync(perm_out, perm64, n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+
+    // ---- columns: staged H2D of the int64 rows (whole tiles per chunk),
+    // checks, re-index; values: checks and indicator classification
+    const int64_t nct = (int64_t)ctseg.size();
+    TileMap col_tm;
+    BK(B.alloc(&col_tm.tb, nct + 1));
+    BK(B.alloc(&col_tm.tseg, std::max<int64_t>(nct, 1)));
+    BK(B.alloc(&col_tm.st0, p + 1));
+    BK(B.alloc(&col_tm.sbeg, std::max<int64_t>(p, 1)));
+    int64_t* col_ptr_d;
+    BK(B.alloc(&col_ptr_d, p + 1));
+    BK(cudaMemcpyAsync(col_tm.tb, ctb.data(), (nct + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    if (nct)
+        BK(cudaMemcpyAsync(col_tm.tseg, ctseg.data(), nct * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(col_tm.st0, cst0.data(), (p + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(col_ptr_d, col_ptr, (p + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    if (p > 0)
+        BK(cudaMemcpyAsync(col_tm.sbeg, col_ptr, p * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    col_tm.ntiles = nct;
+    col_tm.nseg = p;
+    uint32_t *ckey, *ckey2, *vidx = nullptr, *vidx2 = nullptr;
+    BK(B.alloc(&ckey, nnz + 16));  // +16: 16-B-aligned bulk copies of the rows may overhang
+    BK(B.alloc(&ckey2, nnz + 16));
+    const bool has_vals = data->values != nullptr;
+    if (has_vals) {
+        BK(B.alloc(&vidx, nnz));
+        BK(B.alloc(&vidx2, nnz));
+    }
+    if (nnz > 0) {
+        // chunks of whole tiles, about 64 Mi entries each
+        const int64_t per = std::max<int64_t>(1, ((int64_t)1 << 26) / kRxTile);
+        int64_t* stage;
+        BK(B.alloc(&stage, std::min<int64_t>(nnz, per * kRxTile)));
+        for (int64_t t0 = 0; t0 < nct; t0 += per) {
+            const int64_t t1 = std::min(nct, t0 + per);
+            const int64_t e0 = ctb[t0], e1 = ctb[t1];
+            BK(cudaMemcpyAsync(stage, data->row_idx + e0, (e1 - e0) * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, s));
+            const int64_t prev_last = e0 > 0 ? data->row_idx[e0 - 1] : -1;
+            k_b_cols<<<grid_sms(t1 - t0), 256, 0, s>>>(stage, e0, col_tm.tb, t0, t1, col_tm.tseg,
+                                                      col_ptr_d, n, inv, ckey, vidx, prev_last, be);
+            BK(cudaStreamSynchronize(s));  // the stage is refilled next
+        }
+    }
+    double* vals_in = nullptr;
+    uint32_t* nonunit = nullptr;
+    BK(B.alloc(&nonunit, std::max<int64_t>(p, 1)));
+    BK(cudaMemsetAsync(nonunit, 0, std::max<int64_t>(p, 1) * sizeof(uint32_t), s));
+    if (has_vals && nnz > 0) {
+        BK(B.alloc(&vals_in, nnz));
+        BK(cudaMemcpyAsync(vals_in, data->values, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        k_b_vals<<<grid_sms(nct), 256, 0, s>>>(vals_in, col_tm.tb, nct, col_tm.tseg, nonunit, be);
+    }
+    BK(cudaMemcpyAsync(&h, be, sizeof h, cudaMemcpyDeviceToHost, s));
+    std::vector<uint32_t> nonunit_h(std::max<int64_t>(p, 1));
+    BK(cudaMemcpyAsync(nonunit_h.data(), nonunit, nonunit_h.size() * sizeof(uint32_t),
+                       cudaMemcpyDeviceToHost, s));
+    BK(cudaStreamSynchronize(s));
+    if (h.ent_err != kNoErr) {  // data.cpp:55-64, first failing entry and check
+        const int64_t i = (int64_t)(h.ent_err / 4);
+        const int c = (int)(h.ent_err % 4);
+        const int64_t j = std::upper_bound(col_ptr, col_ptr + p + 1, i) - col_ptr - 1;
+        const std::string name = "x" + std::to_string(j + 1);
+        return vfail(ctx, "column " + name +
+                              (c == 0   ? " row indices must be strictly increasing"
+                               : c == 1 ? " row index out of range"
+                                        : " has a non-finite value"));
+    }
+    BK(radix_sort<uint32_t>(ckey, ckey2, vidx, vidx2, has_vals, col_tm, h.r_or ^ h.r_and, hist,
+                            segtot, s));
+    // indicator classification and value compaction (upload_common's rule)
+    std::vector<int64_t> val_off(p, -1);
+    int64_t n_ind = 0, nval = 0;
+    for (int64_t j = 0; j < p; ++j) {
+        if (has_vals && nonunit_h[j]) {
+            val_off[j] = nval;
+            nval += col_ptr[j + 1] - col_ptr[j];
+        } else {
+            ++n_ind;
+        }
+    }
+    int64_t* val_off_d;
+    BK(B.alloc(&val_off_d, std::max<int64_t>(p, 1)));
+    if (p > 0)
+        BK(cudaMemcpyAsync(val_off_d, val_off.data(), p * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    int32_t* rows32 = reinterpret_cast<int32_t*>(ckey);  // sorted rows < 2^31: the int32 view
+    double* vals_c;
+    BK(B.alloc(&vals_c, nval + 16));
+    if (nval > 0)
+        k_b_vals_out<<<grid_sms(nct), 256, 0, s>>>(vidx, vals_in, col_tm.tb, nct, col_tm.tseg,
+                                                  col_ptr_d, val_off_d, vals_c);
+    BK(cudaGetLastError());
+    BK(cudaStreamSynchronize(s));
+    B.release(ckey);
+    B.release(vals_c);
+    return scx_upload_device_design(ctx, n, K, offsets.data(), ev_s, tie_d, p, col_ptr, rows32,
+                                    vals_c, val_off, n_ind);
+}

@@ -265,6 +265,15 @@ struct DesignDev {
     double* gamma;
     double* l2;               // [p] L2 prior weights (extension; zeros unless a prior is given)
     double* trust;
+    // refresh: nonzero-beta columns compacted per refresh and their tile entry
+    // offsets transposed to [tile][active column] (coalesced per tile)
+    int32_t* ref_act;         // [p] active columns, ascending
+    int64_t* ref_abeg;        // [p] their first CSC entry
+    int64_t* ref_avo;         // [p] their value offset (-1 indicator)
+    double* ref_ab;           // [p] their beta
+    int32_t* ref_nact;        // [1] number of active columns
+    int32_t* ref_meta;        // [ntiles1+1][ref_ps] tptr of the active columns, transposed
+    int64_t ref_ps;           // row stride of ref_meta (p rounded up to 32)
     // look-back scratch
     unsigned int* status;     // [ntiles]
     double* slots;            // [2][ntiles][4] agg / inc (s0, s1, s2, flag)
@@ -303,6 +312,8 @@ cudaError_t launch_k2(const DesignDev& d, int fit_mode, cudaStream_t s);
 cudaError_t launch_k3(const DesignDev& d, const ColArgs& col, int mode, double delta,
                       cudaStream_t s);
 // refresh eta/D from beta (make_state / refresh_xbeta)
+// kernels launched by launch_refresh (active columns, their tile table, the tiles, finish)
+constexpr int kRefreshLaunches = 4;
 cudaError_t launch_refresh(const DesignDev& d, cudaStream_t s);
 cudaError_t launch_naive_gh(const DesignDev& d, const ColArgs& col, double* xdense,
                             double* out2, cudaStream_t s);
@@ -325,6 +336,5 @@ cudaError_t launch_narrow_rows(int32_t* dst, const int64_t* src, int64_t count, 
 cudaError_t launch_scan_primitive(const DesignDev& d, double* out, cudaStream_t s);
 cudaError_t launch_k3_sharded(const DesignDev& d, const ColArgs& col, cudaStream_t s);
 const void* k3_apply_ptr();
-const void* refresh_ptr();
 
 }  // namespace scx

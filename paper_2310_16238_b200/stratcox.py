@@ -197,6 +197,20 @@ class DeviceDesign:
     def stream(self) -> int:
         return int(_lib().scx_stream(self._h) or 0)
 
+    def export(self) -> dict:
+        """The device's SortedDesign arrays (scx_design_export): stratum
+        offsets, event, tie_group_end, col_ptr, row_idx (sorted rows), values."""
+        info = self.info()
+        n, k, p, nnz = info["n_rows"], info["n_strata"], info["p"], info["nnz"]
+        off = np.empty(k + 1, np.int64); ev = np.empty(n, np.uint8)
+        te = np.empty(n, np.int64); cp = np.empty(p + 1, np.int64)
+        ri = np.empty(max(nnz, 1), np.int64); va = np.empty(max(nnz, 1), np.float64)
+        _check(_lib().scx_design_export(self._h, ptr(off, C.c_int64), ptr(ev, C.c_uint8),
+                                        ptr(te, C.c_int64), ptr(cp, C.c_int64),
+                                        ptr(ri, C.c_int64), ptr(va, C.c_double)), self._h)
+        return dict(offsets=off, event=ev, tie_end=te, col_ptr=cp, row_idx=ri[:nnz],
+                    values=va[:nnz])
+
     def set_fit_path(self, path: int) -> bool:
         """CCD cycle implementation: 0 automatic (risk-suffix cycle on the chunked
         layout), 1 per-coordinate fused scan only. Returns whether the
