@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests/test_design_build.py tests/test_cv.py tests/test_lowering.py -x -q -p no:cacheprovider > gpurun_out/pytest_build.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_build.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_refresh_tiles -c 1 -o gpurun_out/refresh python scripts/refresh_micro.py --reps 2 > gpurun_out/ncu_refresh.log 2>&1
+timeout 300 python scripts/rs_micro.py --reps 8 > gpurun_out/rs_micro.txt 2>&1
+timeout 900 python -m pytest tests/test_risk_suffix.py tests/test_large_fit.py tests/test_gpu_parity.py -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_c4.log 2>&1
