@@ -16,7 +16,7 @@ LIB       := $(PKG)/libstratcox_b200.so
 CSRC      := $(PKG)/csrc
 OBJDIR    := build/obj
 
-.PHONY: all lib oracle clean dropin
+.PHONY: all lib oracle clean dropin trace
 all: lib oracle
 
 lib: $(LIB)
@@ -47,6 +47,11 @@ $(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o $(OBJDIR)/transforms
 oracle: lib
 	$(MAKE) -C oracle oracle
 	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref && $(MAKE) -C oracle dropin; else echo "reference absent: using prebuilt oracle/_ref if any"; fi
+
+# profiling build: the SCX_K1_DBG traces and timing knobs compiled in (never shipped)
+trace:
+	$(MAKE) NVFLAGS="$(NVFLAGS) -DSCX_TRACE=1" OBJDIR=build/trace LIB=$(PKG)/libstratcox_b200_trace.so \
+	    $(PKG)/libstratcox_b200_trace.so
 
 clean:
 	rm -rf build $(LIB)
