@@ -489,13 +489,11 @@ def main():
     dd = sx.DeviceDesign(design, device=local)
     log(f"[bench] upload {time.perf_counter() - t0:.2f}s info={dd.info()}")
     h = dd.handle
-    if world > 1:
-        from paper_2310_16238_b200.sharding import init_comm
-        init_comm(dd)
     info = dd.info()
     p = design.n_covariates
 
-    # ---- gamma = frac * gamma_max (global across shards)
+    # ---- gamma = frac * gamma_max (global across shards: the ranks' local
+    # gradients at beta = 0 summed, before the shards connect)
     if world == 1:
         gmax = sx.gamma_max(dd)
     else:
@@ -505,6 +503,9 @@ def main():
         gt = torch.tensor(g, device=f"cuda:{local}")
         dist.all_reduce(gt)
         gmax = float(gt.abs().max())
+        del st0
+        from paper_2310_16238_b200.sharding import connect_ipc
+        connect_ipc(dd)  # device-side exchange slots over P2P (NVLink)
     gamma = args.gamma_frac * gmax
     pen = sx.PenaltySpec.shared(p, gamma)
     cfg = sx.OptimizerConfig()
@@ -657,8 +658,8 @@ def main():
         t0 = time.perf_counter()
         dd2 = sx.DeviceDesign(design, device=local)
         if world > 1:
-            from paper_2310_16238_b200.sharding import init_comm
-            init_comm(dd2)
+            from paper_2310_16238_b200.sharding import connect_ipc
+            connect_ipc(dd2)
         r2 = sx.ccd_fit(dd2, pen, cfg)
         barrier()
         el = time.perf_counter() - t0

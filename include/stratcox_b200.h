@@ -307,15 +307,42 @@ int64_t scx_launch_count(const scx_ctx* ctx);
 void* scx_stream(scx_ctx* ctx);
 
 /* ---------------------------------------------------------------- multi-GPU
- * Row-sharded fits: each rank uploads the rows of whole strata it owns
- * (shards split at stratum boundaries, so no scan carry crosses devices) and
- * exchanges the 16-byte (gradient, Hessian) partials per coordinate. The
- * exchange sums partials in rank order, so every rank applies a bit-identical
- * coordinate step. */
-/* 128-byte NCCL unique id, generated on rank 0 and broadcast by the caller. */
-scx_status scx_comm_unique_id(char out[128]);
-scx_status scx_comm_init(scx_ctx* ctx, int nranks, int rank, const char unique_id[128]);
-scx_status scx_comm_destroy(scx_ctx* ctx);
+ * Row-sharded fits: each rank uploads the rows of whole
+ * strata it owns (shards cut at stratum boundaries: no scan carry crosses
+ * ranks), so every rank's risk sets are local; per coordinate the ranks only
+ * exchange a few partial sums. The exchange is device-side, inside the
+ * persistent risk-suffix cycle kernel and a few one-thread kernels, through
+ * 2 x 128-byte slots per rank in device memory that every rank can load:
+ * peer-mapped (P2P over NVLink/NVSwitch) for ranks in one process,
+ * IPC-opened across processes, plain device memory for ranks sharing one
+ * GPU. Partials are summed in rank order, so every rank applies a
+ * bit-identical step; no host round trip per coordinate.
+ * Protocol: [scx_set_sm_budget] -> upload -> scx_xchg_slots / _ipc_handle
+ * -> scx_xchg_connect / _connect_ipc (all ranks) -> combine the ranks'
+ * scx_shard_local_columns (OR nonempty, SUM lin in rank order, MAX xmax,
+ * AND rs_ok) -> scx_shard_set_columns -> scx_ccd_fit on every rank at once.
+ * (Replaces the reference's shared-memory OpenMP parallelism over rows,
+ * scan.cpp:124-190; the reference has no multi-device path.) */
+/* Cycle-kernel CTAs / stratum-aligned chunks (before upload; 0 = every SM):
+ * ranks sharing one GPU split its SMs so their persistent kernels co-reside. */
+scx_status scx_set_sm_budget(scx_ctx* ctx, int sms);
+/* This context's exchange slots (device pointer, zeroed). */
+scx_status scx_xchg_slots(scx_ctx* ctx, void** slots);
+/* The same as a 64-byte cudaIpcMemHandle for other processes. */
+scx_status scx_xchg_ipc_handle(scx_ctx* ctx, char out[64]);
+/* Attach this context as rank `rank` of `nranks` (<= 8): rank_slots[r] =
+ * rank r's slots (rank_slots[rank] = this context's own). Enables P2P to
+ * peer devices. */
+scx_status scx_xchg_connect(scx_ctx* ctx, int nranks, int rank, void* const* rank_slots);
+/* The same from the ranks' IPC handles (handles = nranks x 64 bytes). */
+scx_status scx_xchg_connect_ipc(scx_ctx* ctx, int nranks, int rank, const char* handles);
+/* Per-column facts of this rank's rows: nonempty[p], lin[p] = sum x*delta,
+ * xmax[p] = max |x|; rs_ok: the risk-suffix cycle can run on this shard. */
+scx_status scx_shard_local_columns(scx_ctx* ctx, uint8_t* nonempty, double* lin, double* xmax,
+                                   int* rs_ok);
+/* The combined (global) facts: the same column set, lin and xmax on every rank. */
+scx_status scx_shard_set_columns(scx_ctx* ctx, const uint8_t* nonempty, const double* lin,
+                                 const double* xmax, int rs_ok);
 
 #ifdef __cplusplus
 }

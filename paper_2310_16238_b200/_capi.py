@@ -91,9 +91,13 @@ SIGNATURES = {
     "scx_launch_count": (C.c_int64, [_vp]),
     "scx_debug_k1_trace": (C.c_int, [_i64p]),
     "scx_set_k1_mode": (C.c_int, [_vp, C.c_int, _ip]),
-    "scx_comm_unique_id": (C.c_int, [C.c_char_p]),
-    "scx_comm_init": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
-    "scx_comm_destroy": (C.c_int, [_vp]),
+    "scx_set_sm_budget": (C.c_int, [_vp, C.c_int]),
+    "scx_xchg_slots": (C.c_int, [_vp, C.POINTER(C.c_void_p)]),
+    "scx_xchg_ipc_handle": (C.c_int, [_vp, C.c_char_p]),
+    "scx_xchg_connect": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "scx_xchg_connect_ipc": (C.c_int, [_vp, C.c_int, C.c_int, C.c_char_p]),
+    "scx_shard_local_columns": (C.c_int, [_vp, _i8p, _dp, _dp, C.POINTER(C.c_int)]),
+    "scx_shard_set_columns": (C.c_int, [_vp, _i8p, _dp, _dp, C.c_int]),
 }
 
 class DatasetC(C.Structure):

@@ -5,8 +5,6 @@
 // sequencing on the context's stream, and mapping the device error word back
 // to the reference exception taxonomy (proj/include/stratcox/errors.hpp).
 // No arithmetic of the hot path runs here.
-#include <dlfcn.h>
-
 #include <algorithm>
 #include <array>
 #include <cinttypes>
@@ -26,36 +24,6 @@ using namespace scx;
 namespace {
 
 constexpr long long kNoRow = 0x7fffffffffffffffLL;
-
-// ---------------------------------------------------------------- NCCL (dlopen)
-typedef int ncclResult_t_;
-struct NcclApi {
-    void* h = nullptr;
-    ncclResult_t_ (*GetUniqueId)(void*) = nullptr;
-    ncclResult_t_ (*CommInitRank)(void**, int, char[128], int) = nullptr;
-    ncclResult_t_ (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
-    ncclResult_t_ (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
-    ncclResult_t_ (*CommDestroy)(void*) = nullptr;
-    const char* (*GetErrorString)(ncclResult_t_) = nullptr;
-    bool load() {
-        if (h) return true;
-        const char* names[] = {"libnccl.so.2", "libnccl.so"};
-        for (const char* n : names) {
-            h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
-            if (h) break;
-        }
-        if (!h) return false;
-        GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
-        CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
-        AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
-        AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
-        CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
-        GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
-        return GetUniqueId && CommInitRank && AllGather && AllReduce && CommDestroy;
-    }
-};
-NcclApi g_nccl;
-constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2;
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -133,11 +101,15 @@ struct scx_ctx {
     ColArgs* col1_d = nullptr;        // one column's ColArgs (risk-suffix evaluation)
     int64_t rs_stats[4] = {0, 0, 0, 0};  // last fit: risk-suffix launches, exact hand-offs,
                                          // bound hand-offs, fused-scan cycle launches
-    // multi-GPU
-    void* comm = nullptr;
+    // multi-GPU (row shards): the device exchange (XSlot pairs of every rank,
+    // see internal.cuh) and the global column set
+    Xchg x{};                   // x.nranks == 0 / 1: single device
+    XSlot* xslots = nullptr;    // this rank's two slots
+    std::vector<void*> ipc_open;  // peer slot mappings opened from IPC handles
     int nranks = 1, rank = 0;
-    double* parts_d = nullptr;  // [nranks][4]
+    int sm_budget = 0;          // chunks / co-resident CTAs of the cycle kernel (0: every SM)
     std::vector<uint8_t> gnz;   // column has entries on SOME rank (the sharded loop's column set)
+    std::vector<ColArgs> cycle_cols;  // host copy of cols_d
     Timer timer;
     int64_t launches = 0;  // kernels launched by this context
 };
@@ -171,7 +143,7 @@ void free_design(scx_ctx* ctx) {
     void* ptrs[] = {d.code,   d.D,          d.eta,         d.beta,      d.gamma,     d.l2,
                     d.trust,  d.status,     d.slots,       d.partial,   ctx->xdense,
                     ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
-                    ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, ctx->parts_d, d.lasth1, d.ref_act,
+                    ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, d.lasth1, d.ref_act,
                     d.ref_abeg, d.ref_avo, d.ref_ab, d.ref_nact, d.ref_meta,
                     d.chunk_rows, ctx->cols_d, d.rs_u, d.rs_R, d.rs_Q, d.chunk_k, ctx->col1_d};
     for (void* p : ptrs)
@@ -188,8 +160,8 @@ void free_design(scx_ctx* ctx) {
     ctx->vals_d = nullptr;
     ctx->tptr_d = nullptr;
     ctx->zero_cols_d = nullptr;
-    ctx->parts_d = nullptr;
     ctx->cols_d = nullptr;
+    ctx->cycle_cols.clear();
     ctx->runs.clear();
     ctx->cols.clear();
     ctx->zero_cols.clear();
@@ -301,6 +273,16 @@ scx_status map_error(scx_ctx* ctx, int j_hint) {
         case kErrBadRows:
             snprintf(buf, sizeof buf, "column row indices must be strictly increasing");
             st = SCX_ERR_VALIDATION;
+            break;
+        case kErrXchgTimeout:
+            snprintf(buf, sizeof buf,
+                     "multi-GPU exchange timed out (exchange %lld, site %lld): a peer rank did "
+                     "not arrive", idx / 16, idx % 16);
+            st = SCX_ERR_CUDA;
+            break;
+        case kErrPeer:
+            snprintf(buf, sizeof buf, "another rank of the sharded fit stopped with an error");
+            st = SCX_ERR_CUDA;
             break;
         default:
             snprintf(buf, sizeof buf, "device error kind %d (index %lld)", kind, idx);
@@ -518,8 +500,9 @@ scx_status scx_create(int device, scx_ctx** out) {
 void scx_destroy(scx_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    if (ctx->comm && g_nccl.h) g_nccl.CommDestroy(ctx->comm);
     free_design(ctx);
+    for (void* q : ctx->ipc_open) cudaIpcCloseMemHandle(q);
+    if (ctx->xslots) cudaFree(ctx->xslots);
     if (ctx->d.ctl) cudaFree(ctx->d.ctl);
     if (ctx->out2) cudaFree(ctx->out2);
     if (ctx->warn_d) cudaFree(ctx->warn_d);
@@ -724,6 +707,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        if (ctx->sm_budget > 0) sms = std::min(sms, ctx->sm_budget);  // ranks sharing one GPU
         const int64_t G = sms > 0 ? sms : 148;
         int64_t maxk = 0;
         for (int32_t q = 0; q < k; ++q) maxk = std::max<int64_t>(maxk, offsets[q + 1] - offsets[q]);
@@ -799,6 +783,8 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     {
         int sms = 0, b1 = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        if (ctx->sm_budget > 0) sms = std::min(sms, ctx->sm_budget);
+        d.sm_budget = ctx->sm_budget;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k3_apply_ptr(), kThreads, 0);
         const int per = std::max(1, std::min(b1, 2));
         d.coop_blocks = sms * per;
@@ -833,7 +819,9 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
             CK(cudaMemcpyAsync(ctx->cols_d, nz.data(), nz.size() * sizeof(ColArgs),
                                cudaMemcpyHostToDevice, s));
         CK(cudaStreamSynchronize(s));
+        ctx->cycle_cols = nz;
     }
+    d.x = ctx->x;  // a re-upload keeps the multi-GPU exchange
     CK(dmalloc(&ctx->zero_cols_d, ctx->zero_cols.size()));
     if (!ctx->zero_cols.empty())
         CK(cudaMemcpyAsync(ctx->zero_cols_d, ctx->zero_cols.data(),
@@ -1226,37 +1214,11 @@ static scx_status run_cycle_tail(scx_ctx* ctx, bool end_of_cycle, double* ll, do
     // (optimizer.cpp:103-124); batched at the end of the cycle.
     if (end_of_cycle)
         KL(1, launch_zero_cols(d, ctx->zero_cols_d, (int64_t)ctx->zero_cols.size(), s));
-    if (ctx->nranks > 1) {
-        // log-likelihood and max|eta| are rank-local: gather and reduce in rank order
-        tmark(ctx, 2);
-        KL(1, launch_k2(d, 1, s));
-        tend(ctx);
-        if (scx_status st = read_ctl(ctx)) return st;
-        // (device-side K2 already wrote ll/penalty/mbound into ctl)
-        double send[4] = {ctx->ctl_h->ll, ctx->ctl_h->mbound, 0.0, 0.0};
-        CK(cudaMemcpyAsync(ctx->parts_d + 4 * ctx->rank, send, sizeof send, cudaMemcpyHostToDevice, s));
-        if (g_nccl.AllGather(ctx->parts_d + 4 * ctx->rank, ctx->parts_d, 4, kNcclFloat64, ctx->comm,
-                             s) != 0)
-            return fail(ctx, SCX_ERR_CUDA, "ncclAllGather failed");
-        std::vector<double> all(4 * ctx->nranks);
-        CK(cudaMemcpyAsync(all.data(), ctx->parts_d, all.size() * sizeof(double),
-                           cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        double L = 0.0, M = 0.0;
-        for (int r = 0; r < ctx->nranks; ++r) {
-            L += all[4 * r];
-            M = std::max(M, all[4 * r + 1]);
-        }
-        CK(cudaMemcpyAsync(&d.ctl->mbound, &M, sizeof M, cudaMemcpyHostToDevice, s));
-        if (ctx->ctl_h->err_kind) return map_error(ctx, -1);
-        *ll = L;
-        *pen = ctx->ctl_h->penalty;
-        *max_step = ctx->ctl_h->max_step;
-        return SCX_OK;
-    }
     tmark(ctx, 2);
     KL(1, launch_k2(d, 1, s));
     tend(ctx);
+    // sharded: log L summed over the ranks' rows, max|eta| maxed (rank order)
+    if (ctx->nranks > 1) KL(1, launch_xchg_ctl(d, 1, s));
     if (scx_status st = check_device_error(ctx)) return st;
     *ll = ctx->ctl_h->ll;
     *pen = ctx->ctl_h->penalty;
@@ -1306,22 +1268,22 @@ static scx_status run_coordinate(scx_ctx* ctx, const ColArgs& col) {
         tend(ctx);
         return SCX_OK;
     }
-    // sharded: local partials -> 32-B allgather -> rank-ordered rule -> exact
-    // overflow check with a max-allreduce of the halving level -> apply.
+    // sharded: local (ratio, variance) partials -> device exchange (rank-ordered
+    // sums) + the rule -> the rank's halving level -> max over the ranks ->
+    // apply (a rank without rows of the column still moves beta) -> max|eta|
+    // bound maxed over the ranks (a 256-update refresh may have reset it)
     tmark(ctx, 0);
     KL(1, launch_k1(d, col, kK1Partial, s));
     tend(ctx);
-    if (g_nccl.AllGather(&d.ctl->part[0], ctx->parts_d, 4, kNcclFloat64, ctx->comm, s) != 0)
-        return fail(ctx, SCX_ERR_CUDA, "ncclAllGather failed");
-    KL(1, launch_rank_step(d, col, ctx->parts_d, ctx->nranks, s));
+    KL(1, launch_shard_step(d, col, s));
     ctx->launches += 1;
     k_k3_check<<<std::max(1, (int)std::min<int64_t>((col.nnz + 255) / 256, 1184)), 256, 0, s>>>(
         d.rows, d.vals, d.eta, col, d.ctl);
-    if (g_nccl.AllReduce(&d.ctl->hmax, &d.ctl->hmax, 1, kNcclInt32, kNcclMax, ctx->comm, s) != 0)
-        return fail(ctx, SCX_ERR_CUDA, "ncclAllReduce failed");
+    KL(1, launch_xchg_ctl(d, 2, s));
     tmark(ctx, 1);
     KL(1, launch_k3_sharded(d, col, s));
     tend(ctx);
+    KL(1, launch_xchg_ctl(d, 0, s));
     return SCX_OK;
 }
 
@@ -1391,7 +1353,8 @@ scx_status scx_ccd_fit_prior(scx_ctx* ctx, const double* gamma, const double* l2
     const double zero = 0.0;
     for (int cycle = 1; cycle <= opt->max_cycles; ++cycle) {
         CK(cudaMemcpyAsync(&d.ctl->max_step, &zero, sizeof zero, cudaMemcpyHostToDevice, s));
-        if (ctx->nranks == 1 && !ctx->per_coordinate_fit) {
+        const bool sharded = ctx->nranks > 1;
+        if (!ctx->per_coordinate_fit) {
             // the whole cycle on the device: one cooperative launch per run of
             // same-kind columns (one launch for an all-indicator design)
             // (the risk-suffix cycle when the layout allows it and max|eta| is
@@ -1414,18 +1377,29 @@ scx_status scx_ccd_fit_prior(scx_ctx* ctx, const double* gamma, const double* l2
                         if (why == kRsDone) break;
                         if (why == kRsRefresh) {
                             KL(kRefreshLaunches, launch_refresh(d, s));
+                            if (sharded) KL(1, launch_xchg_ctl(d, 0, s));  // global max|eta|
                             if (scx_status st = check_device_error(ctx)) return st;
                         } else if (why == kRsBound) {
                             ctx->rs_stats[2] += 1;
                         } else if (why == kRsExact) {
                             // this coordinate through the exact fused scan, then resume
                             ctx->rs_stats[1] += 1;
-                            if (scx_status st = fused_cycle(ctx, ctx->cols_d + run[0] + done, 1, run[2] != 0,
-                                                            nullptr))
+                            if (sharded) {
+                                if (scx_status st = run_coordinate(ctx, ctx->cycle_cols[run[0] + done]))
+                                    return st;
+                            } else if (scx_status st = fused_cycle(ctx, ctx->cols_d + run[0] + done, 1,
+                                                                   run[2] != 0, nullptr)) {
                                 return st;
+                            }
                             done += 1;
                         }
                         continue;  // kRsBound: rs_usable() is now false
+                    }
+                    if (sharded) {  // the rest of the run, one coordinate at a time
+                        for (; done < run[1]; ++done)
+                            if (scx_status st = run_coordinate(ctx, ctx->cycle_cols[run[0] + done]))
+                                return st;
+                        break;
                     }
                     int32_t r = 0;
                     if (scx_status st = fused_cycle(ctx, cols, left, run[2] != 0, &r)) return st;
@@ -1533,77 +1507,144 @@ scx_status scx_timing_get(scx_ctx* ctx, int kind, double* total_ms, int64_t* lau
 }
 
 // ---------------------------------------------------------------- multi-GPU
-scx_status scx_comm_unique_id(char out[128]) {
-    if (!g_nccl.load()) return SCX_ERR_CUDA;
-    return g_nccl.GetUniqueId(out) == 0 ? SCX_OK : SCX_ERR_CUDA;
-}
-
-scx_status scx_comm_init(scx_ctx* ctx, int nranks, int rank, const char unique_id[128]) {
-    if (!ctx) return SCX_ERR_VALIDATION;
-    if (nranks < 1 || rank < 0 || rank >= nranks)
-        return fail(ctx, SCX_ERR_VALIDATION, "invalid rank / world size");
-    if (!g_nccl.load()) return fail(ctx, SCX_ERR_CUDA, "libnccl.so.2 not loadable");
-    cudaSetDevice(ctx->device);
-    char id[128];
-    memcpy(id, unique_id, 128);
-    void* comm = nullptr;
-    if (g_nccl.CommInitRank(&comm, nranks, id, rank) != 0)
-        return fail(ctx, SCX_ERR_CUDA, "ncclCommInitRank failed");
-    ctx->comm = comm;
-    ctx->nranks = nranks;
-    ctx->rank = rank;
-    if (ctx->parts_d) cudaFree(ctx->parts_d);
-    CK(dmalloc(&ctx->parts_d, 4 * nranks));
-    // the halving bound must use the global column maxima so that every rank
-    // takes the same decisions
-    if (ctx->has_design && ctx->d.p > 0) {
-        std::vector<double> xm(ctx->d.p);
-        for (int64_t j = 0; j < ctx->d.p; ++j) xm[j] = ctx->cols[j].xmax;
-        double* xm_d = nullptr;
-        CK(dmalloc(&xm_d, ctx->d.p));
-        CK(cudaMemcpyAsync(xm_d, xm.data(), xm.size() * sizeof(double), cudaMemcpyHostToDevice,
-                           ctx->stream));
-        if (g_nccl.AllReduce(xm_d, xm_d, ctx->d.p, kNcclFloat64, kNcclMax, comm, ctx->stream) != 0)
-            return fail(ctx, SCX_ERR_CUDA, "ncclAllReduce failed");
-        CK(cudaMemcpyAsync(xm.data(), xm_d, xm.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        for (int64_t j = 0; j < ctx->d.p; ++j) ctx->cols[j].xmax = xm[j];
-        // which columns have entries on some rank: the global column set, the
-        // same on every rank (zero columns: trust halving at the cycle end)
-        for (int64_t j = 0; j < ctx->d.p; ++j) xm[j] = (double)ctx->cols[j].nnz;
-        CK(cudaMemcpyAsync(xm_d, xm.data(), xm.size() * sizeof(double), cudaMemcpyHostToDevice,
-                           ctx->stream));
-        if (g_nccl.AllReduce(xm_d, xm_d, ctx->d.p, kNcclFloat64, kNcclSum, comm, ctx->stream) != 0)
-            return fail(ctx, SCX_ERR_CUDA, "ncclAllReduce failed");
-        CK(cudaMemcpyAsync(xm.data(), xm_d, xm.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(xm_d);
-        ctx->gnz.assign(ctx->d.p, 0);
-        ctx->zero_cols.clear();
-        for (int64_t j = 0; j < ctx->d.p; ++j) {
-            ctx->gnz[j] = xm[j] > 0.0;
-            if (!ctx->gnz[j]) ctx->zero_cols.push_back((int32_t)j);
-        }
-        if (ctx->zero_cols_d) cudaFree(ctx->zero_cols_d);
-        CK(dmalloc(&ctx->zero_cols_d, ctx->zero_cols.size()));
-        if (!ctx->zero_cols.empty())
-            CK(cudaMemcpyAsync(ctx->zero_cols_d, ctx->zero_cols.data(),
-                               ctx->zero_cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
-                               ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-    }
+// ---------------------------------------------------------------- multi-GPU (row shards)
+scx_status scx_set_sm_budget(scx_ctx* ctx, int sms) {
+    if (!ctx || sms < 0) return SCX_ERR_VALIDATION;
+    ctx->sm_budget = sms;
     return SCX_OK;
 }
 
-scx_status scx_comm_destroy(scx_ctx* ctx) {
-    if (!ctx) return SCX_ERR_VALIDATION;
-    if (ctx->comm && g_nccl.h) g_nccl.CommDestroy(ctx->comm);
-    ctx->comm = nullptr;
-    ctx->nranks = 1;
-    ctx->rank = 0;
-    ctx->gnz.clear();
+scx_status scx_xchg_slots(scx_ctx* ctx, void** slots) {
+    if (!ctx || !slots) return SCX_ERR_VALIDATION;
+    cudaSetDevice(ctx->device);
+    if (!ctx->xslots) CK(cudaMalloc((void**)&ctx->xslots, 2 * sizeof(XSlot)));
+    CK(cudaMemset(ctx->xslots, 0, 2 * sizeof(XSlot)));
+    *slots = ctx->xslots;
+    return SCX_OK;
+}
+
+scx_status scx_xchg_ipc_handle(scx_ctx* ctx, char out[64]) {
+    void* sl = nullptr;
+    if (scx_status st = scx_xchg_slots(ctx, &sl)) return st;
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, sl));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(out, &h, 64);
+    return SCX_OK;
+}
+
+scx_status scx_xchg_connect(scx_ctx* ctx, int nranks, int rank, void* const* rank_slots) {
+    if (!ctx || !rank_slots) return SCX_ERR_VALIDATION;
+    if (nranks < 1 || nranks > kXMaxRanks || rank < 0 || rank >= nranks)
+        return fail(ctx, SCX_ERR_VALIDATION, "invalid rank / world size");
+    cudaSetDevice(ctx->device);
+    void* own = nullptr;
+    if (scx_status st = scx_xchg_slots(ctx, &own)) return st;
+    if (rank_slots[rank] != own)
+        return fail(ctx, SCX_ERR_VALIDATION, "rank_slots[rank] is not this context's exchange slots");
+    Xchg x{};
+    x.nranks = nranks;
+    x.rank = rank;
+    for (int r = 0; r < nranks; ++r) {
+        x.slot[r] = static_cast<XSlot*>(rank_slots[r]);
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, rank_slots[r]) == cudaSuccess && at.device != ctx->device &&
+            at.type == cudaMemoryTypeDevice) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, ctx->device, at.device);
+            if (!can) return fail(ctx, SCX_ERR_CUDA, "peer device not accessible (no P2P)");
+            const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return cuda_fail(ctx, e, "cudaDeviceEnablePeerAccess");
+            cudaGetLastError();
+        }
+    }
+    ctx->x = x;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    ctx->d.x = x;
+    const unsigned long long zero = 0;
+    CK(cudaMemcpy(&ctx->d.ctl->xseq, &zero, sizeof zero, cudaMemcpyHostToDevice));
+    return SCX_OK;
+}
+
+scx_status scx_xchg_connect_ipc(scx_ctx* ctx, int nranks, int rank, const char* handles) {
+    if (!ctx || !handles) return SCX_ERR_VALIDATION;
+    if (nranks < 1 || nranks > kXMaxRanks || rank < 0 || rank >= nranks)
+        return fail(ctx, SCX_ERR_VALIDATION, "invalid rank / world size");
+    cudaSetDevice(ctx->device);
+    void* own = nullptr;
+    if (scx_status st = scx_xchg_slots(ctx, &own)) return st;
+    std::vector<void*> ptrs(nranks, nullptr);
+    for (int r = 0; r < nranks; ++r) {
+        if (r == rank) {
+            ptrs[r] = own;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handles + 64 * r, 64);
+        CK(cudaIpcOpenMemHandle(&ptrs[r], h, cudaIpcMemLazyEnablePeerAccess));
+        ctx->ipc_open.push_back(ptrs[r]);
+    }
+    return scx_xchg_connect(ctx, nranks, rank, ptrs.data());
+}
+
+scx_status scx_shard_local_columns(scx_ctx* ctx, uint8_t* nonempty, double* lin, double* xmax,
+                                   int* rs_ok) {
+    if (scx_status s = need_design(ctx)) return s;
+    for (int64_t j = 0; j < ctx->d.p; ++j) {
+        if (nonempty) nonempty[j] = ctx->cols[j].nnz > 0;
+        if (lin) lin[j] = ctx->cols[j].lin;
+        if (xmax) xmax[j] = ctx->cols[j].xmax;
+    }
+    if (rs_ok) *rs_ok = ctx->d.rs_ok;
+    return SCX_OK;
+}
+
+scx_status scx_shard_set_columns(scx_ctx* ctx, const uint8_t* nonempty, const double* lin,
+                                 const double* xmax, int rs_ok) {
+    if (scx_status s = need_design(ctx)) return s;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const int64_t p = ctx->d.p;
+    ctx->gnz.assign(nonempty, nonempty + p);
+    ctx->zero_cols.clear();
+    for (int64_t j = 0; j < p; ++j) {
+        ctx->cols[j].lin = lin[j];
+        ctx->cols[j].xmax = xmax[j];
+        if (!nonempty[j]) ctx->zero_cols.push_back((int32_t)j);
+    }
+    // the cycle's column set: every globally non-empty column, the same list on
+    // every rank (a rank without rows of a column contributes zero partials)
+    std::vector<ColArgs> nz;
+    ctx->runs.clear();
+    for (int64_t j = 0; j < p; ++j)
+        if (nonempty[j]) {
+            const int32_t ind = ctx->cols[j].indicator;
+            if (ctx->runs.empty() || ctx->runs.back()[2] != ind)
+                ctx->runs.push_back({(int32_t)nz.size(), 0, ind});
+            ctx->runs.back()[1] += 1;
+            nz.push_back(ctx->cols[j]);
+        }
+    if (ctx->cols_d) cudaFree(ctx->cols_d);
+    ctx->cols_d = nullptr;
+    CK(dmalloc(&ctx->cols_d, nz.size()));
+    if (!nz.empty())
+        CK(cudaMemcpyAsync(ctx->cols_d, nz.data(), nz.size() * sizeof(ColArgs), cudaMemcpyHostToDevice, s));
+    ctx->cycle_cols = nz;
+    if (ctx->zero_cols_d) cudaFree(ctx->zero_cols_d);
+    ctx->zero_cols_d = nullptr;
+    CK(dmalloc(&ctx->zero_cols_d, ctx->zero_cols.size()));
+    if (!ctx->zero_cols.empty())
+        CK(cudaMemcpyAsync(ctx->zero_cols_d, ctx->zero_cols.data(),
+                           ctx->zero_cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    ctx->d.rs_ok = ctx->d.rs_ok && rs_ok;
+    CK(cudaStreamSynchronize(s));
+    // every kernel of the sharded fit loaded now, not lazily while a peer spins
+    preload_sharded_kernels(ctx->d);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)k_k3_check);
+    cudaFuncGetAttributes(&fa, (const void*)k_fill);
     return SCX_OK;
 }
 

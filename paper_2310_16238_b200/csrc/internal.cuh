@@ -63,6 +63,8 @@ enum ErrKind : int {
     kErrBadTieEnd = 20,        // validation: tie_group_end out of range (upload)
     kErrBadEvent = 21,         // validation: event indicator must be 0 or 1 (upload)
     kErrBadRows = 22,          // validation: column rows not strictly increasing / out of range
+    kErrXchgTimeout = 30,      // multi-GPU: a peer rank did not reach an exchange in time
+    kErrPeer = 31,             // multi-GPU: another rank stopped with an error
 };
 
 // Control block in device memory (one per context).
@@ -102,6 +104,7 @@ struct DevCtl {
     int pad3;
     int resume;     // cycle kernel: coordinates done before it stopped for a refresh (0: ran to the end)
     int rs_reason;  // risk-suffix cycle: why it stopped (RsStop)
+    unsigned long long xseq;  // multi-GPU: device exchanges done so far (the same on every rank)
 };
 
 // Why a risk-suffix cycle launch returned before its last coordinate.
@@ -238,6 +241,69 @@ __device__ __forceinline__ void set_error(DevCtl* ctl, int kind, long long idx) 
     }
 }
 
+// ------------------------------------------------------------------ device exchange (multi-GPU)
+// Row-sharded fits exchange a few doubles per coordinate: each rank owns two
+// 128-B slots (alternating by exchange number) in device memory that every
+// rank can load — a peer-mapped (P2P over NVLink) or IPC-opened allocation on
+// a node, the same device's memory for ranks sharing one GPU (loopback). The
+// publishing thread writes its values, then the sequence word with release
+// order; readers poll every rank's sequence word and sum (or max) the values
+// in rank order, so every rank computes bit-identical results. Lock-step
+// (every exchange needs every rank) makes two slots enough.
+constexpr int kXMaxRanks = 8;
+constexpr int kXVals = 12;
+struct alignas(128) XSlot {
+    double v[kXVals];
+    int err;                  // the rank stops with an error after this exchange
+    int pad;
+    unsigned long long seq;   // exchange number + 1 once v / err are written
+};
+struct Xchg {
+    XSlot* slot[kXMaxRanks];  // rank r's two slots (slot[rank] = this rank's own)
+    int nranks;               // 1: no exchange
+    int rank;
+};
+
+constexpr long long kXchgTimeoutCycles = 8000000000LL;  // ~4 s: a peer that never comes
+
+// Exchange number k: `publish` (one thread per rank) writes this rank's n
+// values and error flag; every calling thread waits for all ranks and gets
+// the rank-ordered sum (op 0) or max (op 1) in out[] and the OR of the error
+// flags. Returns false on timeout.
+__device__ __forceinline__ bool xchg_values(const Xchg& x, unsigned long long k, const double* mine,
+                                            int n, int op, bool publish, int err_mine, double* out,
+                                            int* err_any) {
+    const int s = (int)(k & 1ull);
+    if (publish) {
+        XSlot* own = x.slot[x.rank] + s;
+        for (int i = 0; i < n; ++i) own->v[i] = mine[i];
+        own->err = err_mine;
+        __threadfence_system();
+        *((volatile unsigned long long*)&own->seq) = k + 1;
+    }
+    const long long t0 = clock64();
+    for (int r = 0; r < x.nranks; ++r) {
+        const volatile unsigned long long* sq = &x.slot[r][s].seq;
+        while (*sq != k + 1) {
+            if (clock64() - t0 > kXchgTimeoutCycles) return false;
+            __nanosleep(64);
+        }
+    }
+    __threadfence_system();
+    int e = 0;
+    for (int i = 0; i < n; ++i) out[i] = op ? 0.0 : 0.0;
+    for (int r = 0; r < x.nranks; ++r) {
+        const XSlot* ps = x.slot[r] + s;
+        for (int i = 0; i < n; ++i) {
+            const double v = __ldcv(&ps->v[i]);
+            out[i] = op ? (r == 0 ? v : fmax(out[i], v)) : (r == 0 ? v : out[i] + v);
+        }
+        e |= __ldcv(&ps->err);
+    }
+    *err_any = e;
+    return true;
+}
+
 // ------------------------------------------------------------------ launch API
 // (defined in kernels.cu; all launches on `stream`)
 struct DesignDev {
@@ -283,6 +349,7 @@ struct DesignDev {
     CUtensorMap tmap_D1;      // box 16 x 128 (2048-row K1 tile)
     CUtensorMap tmap_eta;
     int coop_blocks;          // co-resident blocks for the cooperative kernels
+    int sm_budget;            // SMs of a rank sharing the GPU (0: all)
     // risk-suffix CCD cycle (chunk layout only)
     double* rs_u;             // [npad] scratch: w/S0 per row (forward pass)
     double* rs_R;             // [npad] within-stratum suffix sum of w/S0 from each row
@@ -292,6 +359,7 @@ struct DesignDev {
     CUtensorMap tmap_Q;
     int32_t* chunk_k;         // [nchunks+1] first stratum of each chunk
     int32_t rs_ok;            // chunks hold <= kRsMaxStrata strata each
+    Xchg x;                   // multi-GPU exchange (x.nranks == 1: single device)
 };
 
 enum K1Mode : int { kK1Eval = 0, kK1Fit = 1, kK1Diag = 2, kK1Partial = 3 };
@@ -319,8 +387,11 @@ cudaError_t launch_naive_gh(const DesignDev& d, const ColArgs& col, double* xden
                             double* out2, cudaStream_t s);
 cudaError_t launch_naive_ll(const DesignDev& d, double* out1, cudaStream_t s);
 cudaError_t launch_zero_cols(const DesignDev& d, const int32_t* cols, int64_t ncols, cudaStream_t s);
-cudaError_t launch_rank_step(const DesignDev& d, const ColArgs& col, const double* parts,
-                             int nranks, cudaStream_t s);
+// multi-GPU: rank-summed partials + rule (k_shard_step); ctl exchanges
+// (what 0: max mbound, 1: sum ll + max mbound, 2: max halving level)
+void preload_sharded_kernels(const DesignDev& d);
+cudaError_t launch_shard_step(const DesignDev& d, const ColArgs& col, cudaStream_t s);
+cudaError_t launch_xchg_ctl(const DesignDev& d, int what, cudaStream_t s);
 // design preparation
 cudaError_t launch_build_codes(void* code, int code_bytes, int64_t n, int64_t npad,
                                const uint8_t* event, const int64_t* tie_end,

@@ -128,12 +128,14 @@ class ExecutionConfig:
 class DeviceDesign:
     """A SortedDesign uploaded to one GPU (owns one scx_ctx)."""
 
-    def __init__(self, design: SortedDesign, device: int = 0):
+    def __init__(self, design: SortedDesign, device: int = 0, sm_budget: int = 0):
         lib = _lib()
         h = C.c_void_p()
         rc = lib.scx_create(int(device), C.byref(h))
         if rc != 0:
             raise CudaError(f"scx_create(device={device}) failed: no usable sm_100 device")
+        if sm_budget:
+            lib.scx_set_sm_budget(h, int(sm_budget))
         self._h = h
         self.device = device
         self.design = design
@@ -242,8 +244,8 @@ class DeviceDesign:
         self._state_owner = state
 
 
-def upload(design: SortedDesign, device: int = 0) -> DeviceDesign:
-    return DeviceDesign(design, device)
+def upload(design: SortedDesign, device: int = 0, sm_budget: int = 0) -> DeviceDesign:
+    return DeviceDesign(design, device, sm_budget)
 
 
 class CoefficientState:

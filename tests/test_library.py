@@ -31,7 +31,7 @@ def test_header_declares_the_boundary():
     syms = declared_symbols()
     for must in ("scx_upload_design", "scx_gradient_hessian", "scx_log_partial_likelihood",
                  "scx_update_xbeta", "scx_make_state", "scx_ccd_fit", "scx_segmented_inclusive_scan",
-                 "scx_naive_gradient_hessian", "scx_comm_init"):
+                 "scx_naive_gradient_hessian", "scx_xchg_connect"):
         assert must in syms
 
 

@@ -1,8 +1,9 @@
 """CPU: host logic of the multi-GPU path (rows sharded at stratum boundaries,
 rank-ordered exchange of per-coordinate partials), on gloo with world size 2.
 
-The device exchange runs inside the library over NCCL; here the same
-decomposition is checked with the oracle as the per-shard evaluator:
+The device exchange runs inside the library (tests/test_sharded_fit.py runs
+it on one GPU); here the same decomposition is checked with the oracle as
+the per-shard evaluator:
   * shards start and end on stratum boundaries and cover every row once;
   * the rank-ordered sum of per-shard (gradient, Hessian) partials equals the
     single-design evaluation (1e-12 relative) — no risk set crosses shards;
@@ -145,8 +146,15 @@ def test_sharded_ccd_emulation_gloo_world2():
 
 
 def test_rank_ordered_sum_matches_kernel_order():
-    parts = np.array([[1.0, 3.0, 0.5, 0.0], [2.0, 1.5, 0.25, 0.0], [0.5, 0.25, 1.0, 0.0]])
-    g, h = rank_ordered_sum(parts)
-    lin = (1.0 + 2.0) + 0.5
-    a1 = (3.0 + 1.5) + 0.25
-    assert g == -lin + a1 and h == (0.5 + 0.25) + 1.0
+    parts = np.array([[3.0, 0.5], [1.5, 0.25], [0.25, 1.0]])
+    g, h = rank_ordered_sum(parts, 3.5)
+    assert g == -3.5 + ((3.0 + 1.5) + 0.25) and h == (0.5 + 0.25) + 1.0
+
+
+def test_combine_columns_or_sum_max_and():
+    from paper_2310_16238_b200.sharding import combine_columns
+    f0 = (np.array([1, 0, 0], np.uint8), np.array([1.0, 0.0, 0.0]), np.array([2.0, 0.0, 0.0]), 1)
+    f1 = (np.array([1, 1, 0], np.uint8), np.array([0.5, 2.0, 0.0]), np.array([1.0, 3.0, 0.0]), 0)
+    nz, lin, xmax, ok = combine_columns([f0, f1])
+    assert nz.tolist() == [1, 1, 0] and lin.tolist() == [1.5, 2.0, 0.0]
+    assert xmax.tolist() == [2.0, 3.0, 0.0] and ok == 0
