@@ -1,2 +1,2 @@
-timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_c4.log 2>&1
+free -g > gpurun_out/free.txt; nproc >> gpurun_out/free.txt
+timeout 1500 python scripts/parity_c4_full.py > gpurun_out/parity_full.log 2>&1; echo "rc=$?" >> gpurun_out/parity_full.log
