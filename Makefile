@@ -37,11 +37,15 @@ $(OBJDIR)/design_build.o: $(CSRC)/design_build.cu $(CSRC)/internal.cuh include/s
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/design_build.ptxas.txt || (cat $(OBJDIR)/design_build.ptxas.txt; exit 1)
 
-$(OBJDIR)/transforms.o: $(CSRC)/transforms.cu $(CSRC)/internal.cuh include/stratcox_b200.h
+$(OBJDIR)/io.o: $(CSRC)/io.cpp $(CSRC)/lowered.h include/stratcox_b200.h
+	@mkdir -p $(OBJDIR)
+	g++ -std=c++17 -O3 -fPIC -Wall -c -o $@ $<
+
+$(OBJDIR)/transforms.o: $(CSRC)/transforms.cu $(CSRC)/lowered.h $(CSRC)/internal.cuh include/stratcox_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/transforms.ptxas.txt || (cat $(OBJDIR)/transforms.ptxas.txt; exit 1)
 
-$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o $(OBJDIR)/transforms.o $(OBJDIR)/design_build.o
+$(LIB): $(OBJDIR)/kernels.o $(OBJDIR)/capi.o $(OBJDIR)/cv.o $(OBJDIR)/transforms.o $(OBJDIR)/design_build.o $(OBJDIR)/io.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
 oracle: lib

@@ -279,6 +279,62 @@ scx_status scx_lowered_column_map(const scx_lowered* lowered, int64_t* source, i
                                   double* window_start, double* window_end);
 void scx_lowered_free(scx_lowered* lowered);
 
+/* ---------------------------------------------------------------- files and configuration
+ * io.hpp (proj/src/io.cpp): the two CSV layouts and the key = value config,
+ * same formats, canonical order and error messages as the reference; files
+ * are parsed by a thread pool. Every *err / cap pair receives the message of
+ * a failure (the reference's validation_error text). */
+typedef struct scx_table scx_table;   /* SurvivalDataset + names and stratum labels */
+typedef struct scx_long scx_long;     /* LongData (io.hpp:32-43) */
+typedef struct scx_config scx_config; /* ConfigMap (io.hpp:57-76) */
+/* read_wide_csv (io.cpp:123-193): rows in file order, strata relabelled 1..K
+ * by label (numeric order when every label is a number), columns in name order. */
+scx_status scx_read_wide_csv(const char* path, scx_table** out, char* err, int cap);
+scx_status scx_table_dataset(const scx_table* table, scx_dataset* view);
+const char* scx_table_covariate_name(const scx_table* table, int64_t j);
+int32_t scx_table_n_strata(const scx_table* table);
+const char* scx_table_stratum_label(const scx_table* table, int32_t k); /* k = 1..K */
+void scx_table_free(scx_table* table);
+/* write_wide_csv (io.cpp:195-223); names / labels may be NULL (x1.., 1..). */
+scx_status scx_write_wide_csv(const char* path, const scx_dataset* data,
+                              const char* const* covariate_names, const char* const* stratum_labels,
+                              char* err, int cap);
+/* read_long_csv (io.cpp:225-272) / write_long_csv (io.cpp:274-291). */
+scx_status scx_read_long_csv(const char* path, scx_long** out, char* err, int cap);
+scx_status scx_long_sizes(const scx_long* data, int64_t* n_subjects, int64_t* n_records,
+                          int64_t* n_covariates, double* max_stop);
+const char* scx_long_covariate_name(const scx_long* data, int64_t j);
+scx_status scx_write_long_csv(const char* path, const scx_long* data, char* err, int cap);
+/* to_time_varying (io.cpp:293-345) + lower_pipeline (transforms.cpp:98-231):
+ * the long records' per-interval covariate values, effect-window splits as in
+ * scx_lower_time_varying, augmented to strata (interval-major rows). */
+scx_status scx_long_lower(const scx_long* data, const double* cut_points, int64_t n_cuts,
+                          const int64_t* split_covariate, const int64_t* split_ptr,
+                          const double* split_times, int64_t n_splits, scx_lowered** out,
+                          char* err, int cap);
+void scx_long_free(scx_long* data);
+/* Augmented covariate names of a lowered dataset (window names
+ * "NAME[a-b)" as transforms.cpp:18-21; NULL when the source had no names). */
+const char* scx_lowered_covariate_name(const scx_lowered* lowered, int64_t j);
+/* ConfigMap: from_string / from_file (io.cpp:347-375), typed getters that mark
+ * a key consumed (io.cpp:377-429), finish() naming unconsumed keys (:431-438).
+ * Returned strings live as long as the config. */
+scx_status scx_config_from_string(const char* text, const char* origin, scx_config** out,
+                                  char* err, int cap);
+scx_status scx_config_from_file(const char* path, scx_config** out, char* err, int cap);
+int scx_config_has(const scx_config* config, const char* key);
+const char* scx_config_get_string(scx_config* config, const char* key, const char* fallback);
+scx_status scx_config_get_double(scx_config* config, const char* key, double fallback,
+                                 double* out, char* err, int cap);
+scx_status scx_config_get_int(scx_config* config, const char* key, int64_t fallback,
+                              int64_t* out, char* err, int cap);
+scx_status scx_config_get_double_list(scx_config* config, const char* key, double* out,
+                                      int64_t cap_out, int64_t* n, char* err, int cap);
+/* newline-joined list items; *n = count */
+const char* scx_config_get_string_list(scx_config* config, const char* key, int64_t* n);
+scx_status scx_config_finish(const scx_config* config, char* err, int cap);
+void scx_config_free(scx_config* config);
+
 /* ---------------------------------------------------------------- measurement
  * Device time of the kernels launched by the last call, for bench/roofline:
  * per-kernel-class accumulated milliseconds and launch counts since the last

@@ -116,6 +116,20 @@ class Ref:
             "ref_kfold_select_gamma": (C.c_int, [_vp, _d, C.c_int, _d, C.c_int64, C.c_uint64,
                                                  C.c_int, C.c_double, C.c_double, C.c_int, _d,
                                                  _d, _d, _ip]),
+            "ref_read_wide_csv": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+            "ref_dataset_name": (C.c_char_p, [_vp, C.c_int64]),
+            "ref_dataset_n_labels": (C.c_int32, [_vp]),
+            "ref_dataset_label": (C.c_char_p, [_vp, C.c_int32]),
+            "ref_write_wide_csv": (C.c_int, [_vp, C.c_char_p]),
+            "ref_read_long_csv": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+            "ref_long_sizes": (None, [_vp, _i64, _i64, _i64, _d]),
+            "ref_long_name": (C.c_char_p, [_vp, C.c_int64]),
+            "ref_write_long_csv": (C.c_int, [_vp, C.c_char_p]),
+            "ref_long_free": (None, [_vp]),
+            "ref_long_lower": (C.c_int, [_vp, _d, C.c_int64, _i64, _i64, _d, C.c_int64,
+                                         C.POINTER(_vp), _i64, _i32]),
+            "ref_config_script": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
+                                            C.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -328,6 +342,76 @@ def _ref_resample_methods():
         finally:
             self.L.ref_dataset_free(h)
 
+    # ---- io (proj/src/io.cpp)
+    def read_wide_csv(self, path):
+        """(Dataset, subjects, covariate names, stratum labels) of read_wide_csv."""
+        h = _vp()
+        self._chk(self.L.ref_read_wide_csv(str(path).encode(), C.byref(h)))
+        try:
+            ds = self._dataset(h)
+            subj = np.empty(ds.n, np.int64)
+            self.L.ref_dataset_subject(h, _p(subj, C.c_int64))
+            names = [self.L.ref_dataset_name(h, j).decode() for j in range(ds.p)]
+            labels = [self.L.ref_dataset_label(h, k).decode()
+                      for k in range(1, self.L.ref_dataset_n_labels(h) + 1)]
+            return ds, subj, names, labels
+        finally:
+            self.L.ref_dataset_free(h)
+
+    def wide_roundtrip(self, path_in, path_out):
+        """read_wide_csv + write_wide_csv of the reference."""
+        h = _vp()
+        self._chk(self.L.ref_read_wide_csv(str(path_in).encode(), C.byref(h)))
+        try:
+            self._chk(self.L.ref_write_wide_csv(h, str(path_out).encode()))
+        finally:
+            self.L.ref_dataset_free(h)
+
+    def read_long_csv(self, path):
+        h = _vp()
+        self._chk(self.L.ref_read_long_csv(str(path).encode(), C.byref(h)))
+        return h
+
+    def long_info(self, h):
+        ns = C.c_int64(); nr = C.c_int64(); p = C.c_int64(); mx = C.c_double()
+        self.L.ref_long_sizes(h, C.byref(ns), C.byref(nr), C.byref(p), C.byref(mx))
+        return dict(n_subjects=ns.value, n_records=nr.value, n_covariates=p.value,
+                    max_stop=mx.value,
+                    names=[self.L.ref_long_name(h, j).decode() for j in range(p.value)])
+
+    def long_lower(self, h, cuts, splits=None):
+        """to_time_varying + lower_pipeline: (Dataset, subjects, map_source, map_window, names)."""
+        splits = splits or {}
+        cov = np.array(sorted(splits), np.int64)
+        ptr = np.zeros(len(cov) + 1, np.int64)
+        times = []
+        for q, j in enumerate(cov):
+            times += list(splits[int(j)])
+            ptr[q + 1] = len(times)
+        tm = np.array(times, np.float64) if times else np.zeros(1)
+        cu = np.ascontiguousarray(cuts, np.float64)
+        out = _vp()
+        m = 4096
+        ms = np.zeros(m, np.int64)
+        mw = np.zeros(m, np.int32)
+        self._chk(self.L.ref_long_lower(h, _p(cu, C.c_double), cu.shape[0],
+                                        _p(cov if len(cov) else np.zeros(1, np.int64), C.c_int64),
+                                        _p(ptr, C.c_int64), _p(tm, C.c_double), len(cov),
+                                        C.byref(out), _p(ms, C.c_int64), _p(mw, C.c_int32)))
+        try:
+            low = self._dataset(out)
+            subj = np.empty(low.n, np.int64)
+            self.L.ref_dataset_subject(out, _p(subj, C.c_int64))
+            names = [self.L.ref_dataset_name(out, j).decode() for j in range(low.p)]
+            return low, subj, ms[:low.p], mw[:low.p], names
+        finally:
+            self.L.ref_dataset_free(out)
+
+    def config_script(self, text, script, origin="<config>"):
+        buf = C.create_string_buffer(1 << 16)
+        self.L.ref_config_script(text.encode(), origin.encode(), script.encode(), buf, len(buf))
+        return buf.value.decode()
+
     def lower_pipeline(self, ds, cuts, splits=None, subject=None):
         """make_time_varying + lower_pipeline (transforms.cpp:64-231) of the
         reference; returns (Dataset, subjects, map_source, map_window)."""
@@ -361,6 +445,8 @@ def _ref_resample_methods():
             self.L.ref_dataset_free(h)
 
     Ref.lower_pipeline = lower_pipeline
+    for f in (read_wide_csv, wide_roundtrip, read_long_csv, long_info, long_lower, config_script):
+        setattr(Ref, f.__name__, f)
     Ref.fold_assignment = fold_assignment
     Ref.kfold_select_gamma = kfold_select_gamma
 

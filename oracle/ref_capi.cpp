@@ -31,6 +31,8 @@
 #include "stratcox/optimizer.hpp"
 #include "stratcox/resample.hpp"
 #include "stratcox/transforms.hpp"
+#include "stratcox/io.hpp"
+#include <sstream>
 #include "stratcox/scan.hpp"
 #include "stratcox/simulate.hpp"
 
@@ -474,4 +476,117 @@ int ref_time_fit(void* design, double gamma, int max_cycles, double tolerance, i
     });
 }
 
+
+// ---------------------------------------------------------------- io (proj/src/io.cpp)
+thread_local std::string g_str;
+
+int ref_read_wide_csv(const char* path, void** out) {
+    return guard([&] { *out = new Dataset{read_wide_csv(path), {}}; });
+}
+const char* ref_dataset_name(void* h, int64_t j) {
+    g_str = static_cast<Dataset*>(h)->data.covariate_name(static_cast<std::size_t>(j));
+    return g_str.c_str();
+}
+int32_t ref_dataset_n_labels(void* h) {
+    return static_cast<int32_t>(static_cast<Dataset*>(h)->data.stratum_labels.size());
+}
+const char* ref_dataset_label(void* h, int32_t k) {
+    g_str = static_cast<Dataset*>(h)->data.stratum_label(k);
+    return g_str.c_str();
+}
+int ref_write_wide_csv(void* h, const char* path) {
+    return guard([&] { write_wide_csv(path, static_cast<Dataset*>(h)->data); });
+}
+int ref_read_long_csv(const char* path, void** out) {
+    return guard([&] { *out = new LongData(read_long_csv(path)); });
+}
+void ref_long_sizes(void* h, int64_t* ns, int64_t* nr, int64_t* p, double* max_stop) {
+    const auto& d = *static_cast<LongData*>(h);
+    int64_t r = 0;
+    for (const auto& s : d.subjects) r += static_cast<int64_t>(s.size());
+    *ns = static_cast<int64_t>(d.subjects.size());
+    *nr = r;
+    *p = static_cast<int64_t>(d.covariate_names.size());
+    *max_stop = d.max_stop;
+}
+const char* ref_long_name(void* h, int64_t j) {
+    g_str = static_cast<LongData*>(h)->covariate_names[static_cast<std::size_t>(j)];
+    return g_str.c_str();
+}
+int ref_write_long_csv(void* h, const char* path) {
+    return guard([&] { write_long_csv(path, *static_cast<LongData*>(h)); });
+}
+void ref_long_free(void* h) { delete static_cast<LongData*>(h); }
+// to_time_varying + lower_pipeline; the lowered dataset keeps its covariate names
+int ref_long_lower(void* h, const double* cuts, int64_t n_cuts, const int64_t* split_cov,
+                   const int64_t* split_ptr, const double* split_times, int64_t n_splits,
+                   void** out, int64_t* map_source, int32_t* map_window) {
+    return guard([&] {
+        const auto& d = *static_cast<LongData*>(h);
+        const std::vector<double> cp(cuts, cuts + n_cuts);
+        TimeVaryingDataset tv = to_time_varying(d, cp);
+        TimeVaryingSpec spec;
+        spec.cut_points = cp;
+        for (int64_t s = 0; s < n_splits; ++s) {
+            TimeVaryingSpec::Split sp;
+            sp.covariate = static_cast<std::size_t>(split_cov[s]);
+            sp.times.assign(split_times + split_ptr[s], split_times + split_ptr[s + 1]);
+            spec.splits.push_back(sp);
+        }
+        LoweredDataset low = lower_pipeline(tv, spec);
+        for (std::size_t c = 0; c < low.column_map.size(); ++c) {
+            map_source[c] = static_cast<int64_t>(low.column_map[c].source);
+            map_window[c] = low.column_map[c].window;
+        }
+        *out = new Dataset{std::move(low.data), {}};
+    });
+}
+// ConfigMap driven by a script of "OP key [fallback]" lines (S string, D double,
+// I int, DL double list, SL string list, H has, F finish); one output line per op
+// (results joined by '|', errors as "ERR:<message>"); a from_string failure
+// gives a single "ERR:" line.
+int ref_config_script(const char* text, const char* origin, const char* script, char* out,
+                      int cap) {
+    std::ostringstream res;
+    try {
+        ConfigMap cfg = ConfigMap::from_string(text, origin);
+        std::istringstream sc(script);
+        std::string line;
+        while (std::getline(sc, line)) {
+            std::istringstream ls(line);
+            std::string op, key, fb;
+            ls >> op >> key;
+            std::getline(ls, fb);
+            if (!fb.empty() && fb[0] == ' ') fb.erase(0, 1);
+            try {
+                if (op == "S") {
+                    res << cfg.get_string(key, fb);
+                } else if (op == "D") {
+                    res << format_double(cfg.get_double(key, std::stod(fb)));
+                } else if (op == "I") {
+                    res << cfg.get_int(key, std::stoll(fb));
+                } else if (op == "DL") {
+                    const auto v = cfg.get_double_list(key);
+                    for (std::size_t i = 0; i < v.size(); ++i) res << (i ? "|" : "") << format_double(v[i]);
+                } else if (op == "SL") {
+                    const auto v = cfg.get_string_list(key);
+                    for (std::size_t i = 0; i < v.size(); ++i) res << (i ? "|" : "") << v[i];
+                } else if (op == "H") {
+                    res << (cfg.has(key) ? 1 : 0);
+                } else if (op == "F") {
+                    cfg.finish();
+                    res << "OK";
+                }
+            } catch (const std::exception& e) {
+                res << "ERR:" << e.what();
+            }
+            res << "\n";
+        }
+    } catch (const std::exception& e) {
+        res << "ERR:" << e.what() << "\n";
+    }
+    std::strncpy(out, res.str().c_str(), static_cast<std::size_t>(cap) - 1);
+    out[cap - 1] = 0;
+    return 0;
+}
 }  // extern "C"

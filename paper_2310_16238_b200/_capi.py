@@ -132,6 +132,36 @@ SIGNATURES.update({
     "scx_lowered_dataset": (C.c_int, [_vp, C.POINTER(DatasetC)]),
     "scx_lowered_column_map": (C.c_int, [_vp, _i64p, C.POINTER(C.c_int32), _dp, _dp]),
     "scx_lowered_free": (None, [_vp]),
+    "scx_read_wide_csv": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int]),
+    "scx_table_dataset": (C.c_int, [_vp, C.POINTER(DatasetC)]),
+    "scx_table_covariate_name": (C.c_char_p, [_vp, C.c_int64]),
+    "scx_table_n_strata": (C.c_int32, [_vp]),
+    "scx_table_stratum_label": (C.c_char_p, [_vp, C.c_int32]),
+    "scx_table_free": (None, [_vp]),
+    "scx_write_wide_csv": (C.c_int, [C.c_char_p, C.POINTER(DatasetC), C.POINTER(C.c_char_p),
+                                     C.POINTER(C.c_char_p), C.c_char_p, C.c_int]),
+    "scx_read_long_csv": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int]),
+    "scx_long_sizes": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int64), _dp]),
+    "scx_long_covariate_name": (C.c_char_p, [_vp, C.c_int64]),
+    "scx_write_long_csv": (C.c_int, [C.c_char_p, _vp, C.c_char_p, C.c_int]),
+    "scx_long_lower": (C.c_int, [_vp, _dp, C.c_int64, _i64p, _i64p, _dp, C.c_int64,
+                                 C.POINTER(C.c_void_p), C.c_char_p, C.c_int]),
+    "scx_long_free": (None, [_vp]),
+    "scx_lowered_covariate_name": (C.c_char_p, [_vp, C.c_int64]),
+    "scx_config_from_string": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p),
+                                         C.c_char_p, C.c_int]),
+    "scx_config_from_file": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_int]),
+    "scx_config_has": (C.c_int, [_vp, C.c_char_p]),
+    "scx_config_get_string": (C.c_char_p, [_vp, C.c_char_p, C.c_char_p]),
+    "scx_config_get_double": (C.c_int, [_vp, C.c_char_p, C.c_double, _dp, C.c_char_p, C.c_int]),
+    "scx_config_get_int": (C.c_int, [_vp, C.c_char_p, C.c_int64, C.POINTER(C.c_int64),
+                                     C.c_char_p, C.c_int]),
+    "scx_config_get_double_list": (C.c_int, [_vp, C.c_char_p, _dp, C.c_int64,
+                                             C.POINTER(C.c_int64), C.c_char_p, C.c_int]),
+    "scx_config_get_string_list": (C.c_char_p, [_vp, C.c_char_p, C.POINTER(C.c_int64)]),
+    "scx_config_finish": (C.c_int, [_vp, C.c_char_p, C.c_int]),
+    "scx_config_free": (None, [_vp]),
     "scx_kfold_select_gamma": (C.c_int, [C.POINTER(DatasetC), _dp, C.POINTER(CvConfigC),
                                          C.POINTER(FitOptions), C.POINTER(C.c_int), C.c_int,
                                          C.POINTER(CvResultC), C.c_char_p, C.c_int]),

@@ -1,0 +1,22 @@
+// Library-owned lowered dataset (scx_lowered in include/stratcox_b200.h):
+// the augmented SurvivalDataset of lower_pipeline (transforms.cpp:225-231)
+// and its column map. Shared by transforms.cu (time-fixed subjects) and
+// io.cpp (long-format files with time-varying covariates).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+struct scx_lowered {
+    std::vector<double> time;
+    std::vector<uint8_t> event;
+    std::vector<int32_t> stratum;
+    std::vector<int64_t> subject;
+    std::vector<int64_t> col_ptr;
+    std::vector<int64_t> rows;
+    std::vector<double> values;
+    std::vector<int64_t> map_source;
+    std::vector<int32_t> map_window;
+    std::vector<double> map_start, map_end;
+    std::vector<std::string> names;  // augmented covariate names (empty: x1..xP)
+};

@@ -25,18 +25,7 @@
 
 #include "../../include/stratcox_b200.h"
 
-struct scx_lowered {
-    std::vector<double> time;
-    std::vector<uint8_t> event;
-    std::vector<int32_t> stratum;
-    std::vector<int64_t> subject;
-    std::vector<int64_t> col_ptr;
-    std::vector<int64_t> rows;
-    std::vector<double> values;
-    std::vector<int64_t> map_source;
-    std::vector<int32_t> map_window;
-    std::vector<double> map_start, map_end;
-};
+#include "lowered.h"
 
 namespace {
 
