@@ -33,7 +33,7 @@ $(OBJDIR)/cv.o: $(CSRC)/cv.cu $(CSRC)/internal.cuh include/stratcox_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/cv.ptxas.txt || (cat $(OBJDIR)/cv.ptxas.txt; exit 1)
 
-$(OBJDIR)/design_build.o: $(CSRC)/design_build.cu $(CSRC)/internal.cuh include/stratcox_b200.h
+$(OBJDIR)/design_build.o: $(CSRC)/design_build.cu $(CSRC)/internal.cuh $(CSRC)/lowered.h include/stratcox_b200.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(ARCH) $(NVFLAGS) -c -o $@ $< 2> $(OBJDIR)/design_build.ptxas.txt || (cat $(OBJDIR)/design_build.ptxas.txt; exit 1)
 

@@ -222,6 +222,22 @@ typedef struct {
  * may be NULL: sorted row s is input row perm_out[s]. */
 scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, int64_t* perm_out);
 
+/* Lowering + build on the device (BASELINE configs 2-3; PAPER.md:582-583
+ * "mappings on the original data" instead of duplication): only the
+ * SUBJECT-level data (scx_dataset over subjects, time-fixed covariates) is
+ * uploaded; the subject x interval -> augmented-row mapping, the augmented
+ * rows and columns (augment_to_strata + split_time_varying_coefficient,
+ * transforms.cpp:98-223, same arrays as scx_lower_time_varying) and then
+ * build_sorted_design run on the device. The duplicated design never exists
+ * on the host. map_* [p_out] (may be NULL) receive the column map,
+ * p_out = p + sum over splits of their number of times. */
+scx_status scx_build_lowered_design(scx_ctx* ctx, const scx_dataset* subjects,
+                                    const double* cut_points, int64_t n_cuts,
+                                    const int64_t* split_covariate, const int64_t* split_ptr,
+                                    const double* split_times, int64_t n_splits,
+                                    int64_t* perm_out, int64_t* map_source, int32_t* map_window,
+                                    double* map_start, double* map_end);
+
 /* default_gamma_grid (resample.hpp:42, resample.cpp:57-68): `size` values
  * log-spaced over [gamma_max / 1e4, gamma_max]. */
 scx_status scx_default_gamma_grid(double gamma_max, int64_t size, double* out);

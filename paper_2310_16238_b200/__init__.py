@@ -26,6 +26,7 @@ from .stratcox import (  # noqa: F401
     SurvivalDataset,
     apply_trust_region,
     build_design,
+    build_lowered_design,
     ccd_fit,
     fold_assignment,
     kfold_select_gamma,

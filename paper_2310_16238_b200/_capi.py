@@ -124,6 +124,9 @@ class CvResultC(C.Structure):
 SIGNATURES.update({
     "scx_build_design": (C.c_int, [_vp, C.POINTER(DatasetC), _i64p]),
     "scx_default_gamma_grid": (C.c_int, [C.c_double, C.c_int64, _dp]),
+    "scx_build_lowered_design": (C.c_int, [_vp, C.POINTER(DatasetC), _dp, C.c_int64, _i64p, _i64p,
+                                           _dp, C.c_int64, _i64p, _i64p, C.POINTER(C.c_int32),
+                                           _dp, _dp]),
     "scx_fold_assignment": (C.c_int, [C.POINTER(DatasetC), C.c_int, C.c_uint64,
                                       C.POINTER(C.c_int32)]),
     "scx_lower_time_varying": (C.c_int, [C.POINTER(DatasetC), _dp, C.c_int64, _i64p, _i64p, _dp,

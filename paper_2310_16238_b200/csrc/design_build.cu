@@ -32,6 +32,7 @@
 
 #include "../../include/stratcox_b200.h"
 #include "internal.cuh"
+#include "lowered.h"
 
 namespace scx {
 
@@ -466,6 +467,198 @@ __global__ void k_b_vals_out(const uint32_t* vidx, const double* vals, const int
     }
 }
 
+// ---------------------------------------------------------------- device lowering
+// augment_to_strata (transforms.cpp:177-223) from the SUBJECT-level data: the
+// host uploads the original (un-duplicated) subjects and the mapping subject x
+// interval -> augmented row is evaluated here, so the duplicated design only
+// ever exists in HBM ("mappings on the original data").
+__device__ __forceinline__ int lw_event_interval(double y, const double* cuts, int K) {
+    if (y == cuts[K]) return K;
+    int lo = 0, hi = K + 1;  // upper_bound over cuts[0..K]
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cuts[mid] <= y)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ bool lw_at_risk(double y, uint8_t ev, int k, const double* cuts, int K) {
+    if (y > cuts[k - 1]) return true;  // transforms.cpp:32-36
+    return ev != 0 && y == cuts[k - 1] && lw_event_interval(y, cuts, K) == k;
+}
+
+// flag[(k-1) n + i] = subject i at risk in interval k (interval-major = output row order)
+__global__ void k_lw_flags(const double* time, const uint8_t* event, int64_t n, const double* cuts,
+                           int K, uint32_t* flag) {
+    const int64_t m = (int64_t)K * n;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(t / n) + 1;
+        const int64_t i = t - (int64_t)(k - 1) * n;
+        flag[t] = lw_at_risk(time[i], event[i], k, cuts, K) ? 1u : 0u;
+    }
+}
+
+// exclusive scan of m u32 values in place (1024 per block), block totals out
+constexpr int kScanB = 1024;
+__global__ void __launch_bounds__(kScanB) k_scan_blocks(uint32_t* v, int64_t m, uint32_t* tot) {
+    __shared__ uint32_t ws[32];
+    const int64_t i = (int64_t)blockIdx.x * kScanB + threadIdx.x;
+    const uint32_t x = i < m ? v[i] : 0u;
+    uint32_t inc = x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = ws[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        ws[lane] = t;
+    }
+    __syncthreads();
+    const uint32_t ex = inc - x + (w ? ws[w - 1] : 0u);
+    if (i < m) v[i] = ex;
+    if (threadIdx.x == kScanB - 1) tot[blockIdx.x] = ws[31];
+}
+// one block: exclusive scan of the block totals in chunks (carry between chunks)
+__global__ void __launch_bounds__(kScanB) k_scan_tops(uint32_t* tot, int64_t nb, uint32_t* total) {
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t b0 = 0; b0 < nb; b0 += kScanB) {
+        const int64_t i = b0 + threadIdx.x;
+        const uint32_t x = i < nb ? tot[i] : 0u;
+        uint32_t inc = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) ws[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t t = ws[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            ws[lane] = t;
+        }
+        __syncthreads();
+        const uint32_t c0 = carry;
+        if (i < nb) tot[i] = c0 + inc - x + (w ? ws[w - 1] : 0u);
+        __syncthreads();
+        if (threadIdx.x == 0) carry = c0 + ws[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+__global__ void k_scan_add(uint32_t* v, int64_t m, const uint32_t* tot) {
+    const int64_t i = (int64_t)blockIdx.x * kScanB + threadIdx.x;
+    if (i < m) v[i] += tot[blockIdx.x];
+}
+
+// augmented rows (interval-major; subjects in input order inside an interval)
+__global__ void k_lw_rows(const double* time, const uint8_t* event, const int64_t* subject,
+                          int64_t n, const double* cuts, int K, const uint32_t* flag0,
+                          const uint32_t* idx, double* a_time, uint8_t* a_event, int32_t* a_str,
+                          int64_t* a_subj) {
+    const int64_t m = (int64_t)K * n;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < m;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(t / n) + 1;
+        const int64_t i = t - (int64_t)(k - 1) * n;
+        const double y = time[i];
+        if (!lw_at_risk(y, event[i], k, cuts, K)) continue;
+        const uint32_t r = idx[t];
+        a_time[r] = fmin(y, cuts[k]);
+        a_event[r] = event[i] && lw_event_interval(y, cuts, K) == k ? 1 : 0;
+        a_str[r] = k;
+        a_subj[r] = subject ? subject[i] : i + 1;
+    }
+}
+
+// per (output column c, interval k): the source column's entries whose subject
+// is at risk in k (and value != 0), counted, then written in entry order
+struct LwCol {
+    int64_t beg, end;  // source entries
+    double start, stop;
+    int window;
+    int pad;
+};
+__global__ void k_lw_count(const LwCol* cols, const int64_t* rows, const double* vals,
+                           const uint32_t* flag0_unused, const double* cuts, int K, int64_t n,
+                           const uint32_t* at_risk, uint32_t* cnt) {
+    const int c = blockIdx.y, k = blockIdx.x + 1;
+    const LwCol col = cols[c];
+    uint32_t m = 0;
+    if (col.window < 0 || (cuts[k - 1] >= col.start && cuts[k - 1] < col.stop))
+        for (int64_t t = col.beg + threadIdx.x; t < col.end; t += blockDim.x) {
+            const double v = vals ? vals[t] : 1.0;
+            m += (v != 0.0 && at_risk[(int64_t)(k - 1) * n + rows[t]]) ? 1u : 0u;
+        }
+    for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+    __shared__ uint32_t ws[32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t a = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += ws[w];
+        cnt[(int64_t)c * K + (k - 1)] = a;
+    }
+}
+__global__ void __launch_bounds__(256) k_lw_fill(const LwCol* cols, const int64_t* rows,
+                                                 const double* vals, const double* cuts, int K,
+                                                 int64_t n, const uint32_t* at_risk,
+                                                 const uint32_t* idx, const int64_t* off,
+                                                 int64_t* out_rows, double* out_vals) {
+    const int c = blockIdx.y, k = blockIdx.x + 1;
+    const LwCol col = cols[c];
+    if (!(col.window < 0 || (cuts[k - 1] >= col.start && cuts[k - 1] < col.stop))) return;
+    __shared__ uint32_t ws[8];
+    __shared__ int64_t base;
+    if (threadIdx.x == 0) base = off[(int64_t)c * K + (k - 1)];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t t0 = col.beg; t0 < col.end; t0 += 256) {
+        const int64_t t = t0 + threadIdx.x;
+        bool on = false;
+        int64_t r = 0;
+        double v = 1.0;
+        if (t < col.end) {
+            v = vals ? vals[t] : 1.0;
+            const int64_t q = (int64_t)(k - 1) * n + rows[t];
+            on = v != 0.0 && at_risk[q];
+            if (on) r = idx[q];
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) ws[w] = __popc(bal);
+        __syncthreads();
+        uint32_t before = 0, all = 0;
+        for (int q = 0; q < 8; ++q) {
+            before += q < w ? ws[q] : 0u;
+            all += ws[q];
+        }
+        if (on) {
+            const int64_t pos = base + before + __popc(bal & ((1u << lane) - 1u));
+            out_rows[pos] = r;
+            if (out_vals) out_vals[pos] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) base += all;
+        __syncthreads();
+    }
+}
+
 }  // namespace scx
 
 // ---------------------------------------------------------------- host driver
@@ -535,16 +728,38 @@ static scx_status vfail(scx_ctx* ctx, const std::string& m) {
     return SCX_ERR_VALIDATION;
 }
 
+// Input of the build: host arrays (scx_build_design) or device arrays (the
+// device lowering, scx_build_lowered_design). col_ptr is always on the host.
+struct BuildIn {
+    int64_t n, p;
+    const double* time;
+    const uint8_t* event;
+    const int32_t* stratum;
+    const int64_t* col_ptr;
+    const int64_t* rows;
+    const double* values;  // NULL: every value 1.0
+    bool device;           // time / event / stratum / rows / values are device pointers
+};
+
+static scx_status build_core(scx_ctx* ctx, const BuildIn& in, int64_t* perm_out);
+
 extern "C" scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, int64_t* perm_out) {
     if (!ctx || !data) return SCX_ERR_VALIDATION;
+    const BuildIn in{data->n_rows, data->n_covariates, data->time, data->event, data->stratum,
+                     data->col_ptr, data->row_idx, data->values, false};
+    return build_core(ctx, in, perm_out);
+}
+
+static scx_status build_core(scx_ctx* ctx, const BuildIn& in, int64_t* perm_out) {
+    BuildIn data = in;
     cudaSetDevice(scx_ctx_device(ctx));
     cudaStream_t s = scx_ctx_stream(ctx);
-    const int64_t n = data->n_rows, p = data->n_covariates;
+    const int64_t n = data.n, p = data.p;
     if (n == 0) return vfail(ctx, "dataset has no rows");
     if (n < 0 || p < 0) return vfail(ctx, "negative dataset size");
     if (n > (int64_t)0x7fffffff - kTileRows)
         return vfail(ctx, "row count exceeds the int32 row-index range");
-    const int64_t* col_ptr = data->col_ptr;
+    const int64_t* col_ptr = data.col_ptr;
     if (col_ptr[0] != 0) return vfail(ctx, "col_ptr[0] must be 0");
     for (int64_t j = 0; j < p; ++j)
         if (col_ptr[j + 1] < col_ptr[j]) return vfail(ctx, "col_ptr must be non-decreasing");
@@ -556,13 +771,19 @@ extern "C" scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, in
     uint8_t* event_d;
     int32_t* str_d;
     BuildErr* be;
-    BK(B.alloc(&time_d, n));
-    BK(B.alloc(&event_d, n));
-    BK(B.alloc(&str_d, n));
     BK(B.alloc(&be, 1));
-    BK(cudaMemcpyAsync(time_d, data->time, n * sizeof(double), cudaMemcpyHostToDevice, s));
-    BK(cudaMemcpyAsync(event_d, data->event, n, cudaMemcpyHostToDevice, s));
-    BK(cudaMemcpyAsync(str_d, data->stratum, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    if (data.device) {
+        time_d = const_cast<double*>(data.time);
+        event_d = const_cast<uint8_t*>(data.event);
+        str_d = const_cast<int32_t*>(data.stratum);
+    } else {
+        BK(B.alloc(&time_d, n));
+        BK(B.alloc(&event_d, n));
+        BK(B.alloc(&str_d, n));
+        BK(cudaMemcpyAsync(time_d, data.time, n * sizeof(double), cudaMemcpyHostToDevice, s));
+        BK(cudaMemcpyAsync(event_d, data.event, n, cudaMemcpyHostToDevice, s));
+        BK(cudaMemcpyAsync(str_d, data.stratum, n * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
     {
         BuildErr init;
         std::memset(&init, 0, sizeof init);
@@ -691,12 +912,15 @@ extern "C" scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, in
     uint32_t *ckey, *ckey2, *vidx = nullptr, *vidx2 = nullptr;
     BK(B.alloc(&ckey, nnz + 16));  // +16: 16-B-aligned bulk copies of the rows may overhang
     BK(B.alloc(&ckey2, nnz + 16));
-    const bool has_vals = data->values != nullptr;
+    const bool has_vals = data.values != nullptr;
     if (has_vals) {
         BK(B.alloc(&vidx, nnz));
         BK(B.alloc(&vidx2, nnz));
     }
-    if (nnz > 0) {
+    if (nnz > 0 && data.device) {  // device rows: one pass over every tile
+        k_b_cols<<<grid_sms(nct), 256, 0, s>>>(data.rows, 0, col_tm.tb, 0, nct, col_tm.tseg, col_ptr_d,
+                                              n, inv, ckey, vidx, -1, be);
+    } else if (nnz > 0) {
         // chunks of whole tiles, about 64 Mi entries each
         const int64_t per = std::max<int64_t>(1, ((int64_t)1 << 26) / kRxTile);
         int64_t* stage;
@@ -704,9 +928,9 @@ extern "C" scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, in
         for (int64_t t0 = 0; t0 < nct; t0 += per) {
             const int64_t t1 = std::min(nct, t0 + per);
             const int64_t e0 = ctb[t0], e1 = ctb[t1];
-            BK(cudaMemcpyAsync(stage, data->row_idx + e0, (e1 - e0) * sizeof(int64_t),
+            BK(cudaMemcpyAsync(stage, data.rows + e0, (e1 - e0) * sizeof(int64_t),
                                cudaMemcpyHostToDevice, s));
-            const int64_t prev_last = e0 > 0 ? data->row_idx[e0 - 1] : -1;
+            const int64_t prev_last = e0 > 0 ? data.rows[e0 - 1] : -1;
             k_b_cols<<<grid_sms(t1 - t0), 256, 0, s>>>(stage, e0, col_tm.tb, t0, t1, col_tm.tseg,
                                                       col_ptr_d, n, inv, ckey, vidx, prev_last, be);
             BK(cudaStreamSynchronize(s));  // the stage is refilled next
@@ -717,8 +941,12 @@ extern "C" scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, in
     BK(B.alloc(&nonunit, std::max<int64_t>(p, 1)));
     BK(cudaMemsetAsync(nonunit, 0, std::max<int64_t>(p, 1) * sizeof(uint32_t), s));
     if (has_vals && nnz > 0) {
-        BK(B.alloc(&vals_in, nnz));
-        BK(cudaMemcpyAsync(vals_in, data->values, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (data.device) {
+            vals_in = const_cast<double*>(data.values);
+        } else {
+            BK(B.alloc(&vals_in, nnz));
+            BK(cudaMemcpyAsync(vals_in, data.values, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
         k_b_vals<<<grid_sms(nct), 256, 0, s>>>(vals_in, col_tm.tb, nct, col_tm.tseg, nonunit, be);
     }
     BK(cudaMemcpyAsync(&h, be, sizeof h, cudaMemcpyDeviceToHost, s));
@@ -765,4 +993,129 @@ extern "C" scx_status scx_build_design(scx_ctx* ctx, const scx_dataset* data, in
     B.release(vals_c);
     return scx_upload_device_design(ctx, n, K, offsets.data(), ev_s, tie_d, p, col_ptr, rows32,
                                     vals_c, val_off, n_ind);
+}
+
+
+// ---------------------------------------------------------------- device lowering + build
+extern "C" scx_status scx_build_lowered_design(scx_ctx* ctx, const scx_dataset* subjects,
+                                               const double* cut_points, int64_t n_cuts,
+                                               const int64_t* split_covariate,
+                                               const int64_t* split_ptr, const double* split_times,
+                                               int64_t n_splits, int64_t* perm_out,
+                                               int64_t* map_source, int32_t* map_window,
+                                               double* map_start, double* map_end) {
+    if (!ctx || !subjects || !cut_points) return SCX_ERR_VALIDATION;
+    std::vector<LowerCol> plan;
+    std::string why;
+    if (!lowering_plan(subjects, cut_points, n_cuts, split_covariate, split_ptr, split_times,
+                       n_splits, plan, why))
+        return vfail(ctx, why);
+    cudaSetDevice(scx_ctx_device(ctx));
+    cudaStream_t s = scx_ctx_stream(ctx);
+    const int64_t n = subjects->n_rows, p = subjects->n_covariates;
+    const int K = (int)n_cuts - 1;
+    const int64_t* cp = subjects->col_ptr;
+    const int64_t nnz = cp[p];
+    const int64_t pc = (int64_t)plan.size();
+    for (int64_t c = 0; c < pc; ++c) {
+        if (map_source) map_source[c] = plan[c].src;
+        if (map_window) map_window[c] = plan[c].window;
+        if (map_start) map_start[c] = plan[c].start;
+        if (map_end) map_end[c] = plan[c].end;
+    }
+    if ((int64_t)K * n >= ((int64_t)1 << 32))
+        return vfail(ctx, "subjects x intervals exceeds the 32-bit row range");
+    DevBuf B;
+    // the subject-level (un-duplicated) data goes to the device once
+    double *time_d, *cuts_d, *vals_d = nullptr;
+    uint8_t* event_d;
+    int64_t *subj_d = nullptr, *rows_d;
+    BK(B.alloc(&time_d, n));
+    BK(B.alloc(&event_d, n));
+    BK(B.alloc(&cuts_d, n_cuts));
+    BK(B.alloc(&rows_d, std::max<int64_t>(nnz, 1)));
+    BK(cudaMemcpyAsync(time_d, subjects->time, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(event_d, subjects->event, n, cudaMemcpyHostToDevice, s));
+    BK(cudaMemcpyAsync(cuts_d, cut_points, n_cuts * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (nnz)
+        BK(cudaMemcpyAsync(rows_d, subjects->row_idx, nnz * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    if (subjects->subject) {
+        BK(B.alloc(&subj_d, n));
+        BK(cudaMemcpyAsync(subj_d, subjects->subject, n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    }
+    if (subjects->values && nnz) {
+        BK(B.alloc(&vals_d, nnz));
+        BK(cudaMemcpyAsync(vals_d, subjects->values, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    // mapping subject x interval -> augmented row: at-risk flags, exclusive scan
+    const int64_t m = (int64_t)K * n;
+    uint32_t *flag, *idx, *tot, *na_d;
+    BK(B.alloc(&flag, m));
+    BK(B.alloc(&idx, m));
+    const int64_t nb = (m + kScanB - 1) / kScanB;
+    BK(B.alloc(&tot, nb));
+    BK(B.alloc(&na_d, 1));
+    const int gm = grid_sms((m + 255) / 256);
+    k_lw_flags<<<gm, 256, 0, s>>>(time_d, event_d, n, cuts_d, K, flag);
+    BK(cudaMemcpyAsync(idx, flag, m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    k_scan_blocks<<<(unsigned)nb, kScanB, 0, s>>>(idx, m, tot);
+    k_scan_tops<<<1, kScanB, 0, s>>>(tot, nb, na_d);
+    k_scan_add<<<(unsigned)nb, kScanB, 0, s>>>(idx, m, tot);
+    uint32_t na = 0;
+    BK(cudaMemcpyAsync(&na, na_d, sizeof na, cudaMemcpyDeviceToHost, s));
+    BK(cudaStreamSynchronize(s));
+    const int64_t N = na;
+    if (N == 0) return vfail(ctx, "dataset has no rows");
+    double* a_time;
+    uint8_t* a_event;
+    int32_t* a_str;
+    int64_t* a_subj;
+    BK(B.alloc(&a_time, N));
+    BK(B.alloc(&a_event, N));
+    BK(B.alloc(&a_str, N));
+    BK(B.alloc(&a_subj, N));
+    k_lw_rows<<<gm, 256, 0, s>>>(time_d, event_d, subj_d, n, cuts_d, K, flag, idx, a_time, a_event,
+                                 a_str, a_subj);
+    // the augmented columns: per (column, interval) counts -> offsets -> entries
+    std::vector<LwCol> lc(pc);
+    for (int64_t c = 0; c < pc; ++c)
+        lc[c] = LwCol{cp[plan[c].src], cp[plan[c].src + 1], plan[c].start, plan[c].end,
+                      plan[c].window, 0};
+    LwCol* lc_d;
+    uint32_t* cnt_d;
+    BK(B.alloc(&lc_d, std::max<int64_t>(pc, 1)));
+    BK(B.alloc(&cnt_d, std::max<int64_t>(pc * K, 1)));
+    std::vector<int64_t> acp(pc + 1, 0);
+    std::vector<int64_t> off(std::max<int64_t>(pc * K, 1), 0);
+    if (pc > 0) {
+        BK(cudaMemcpyAsync(lc_d, lc.data(), pc * sizeof(LwCol), cudaMemcpyHostToDevice, s));
+        k_lw_count<<<dim3((unsigned)K, (unsigned)pc), 256, 0, s>>>(lc_d, rows_d, vals_d, nullptr, cuts_d,
+                                                                  K, n, flag, cnt_d);
+        std::vector<uint32_t> cnt(pc * K);
+        BK(cudaMemcpyAsync(cnt.data(), cnt_d, pc * K * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        BK(cudaStreamSynchronize(s));
+        for (int64_t c = 0; c < pc; ++c) {
+            int64_t run = acp[c];
+            for (int k = 0; k < K; ++k) {
+                off[c * K + k] = run;
+                run += cnt[c * K + k];
+            }
+            acp[c + 1] = run;
+        }
+    }
+    const int64_t annz = acp[pc];
+    int64_t *a_rows, *off_d;
+    double* a_vals = nullptr;
+    BK(B.alloc(&a_rows, std::max<int64_t>(annz, 1)));
+    BK(B.alloc(&off_d, std::max<int64_t>(pc * K, 1)));
+    if (vals_d) BK(B.alloc(&a_vals, std::max<int64_t>(annz, 1)));
+    if (pc > 0) {
+        BK(cudaMemcpyAsync(off_d, off.data(), pc * K * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        k_lw_fill<<<dim3((unsigned)K, (unsigned)pc), 256, 0, s>>>(lc_d, rows_d, vals_d, cuts_d, K, n,
+                                                                 flag, idx, off_d, a_rows, a_vals);
+    }
+    BK(cudaGetLastError());
+    // ... and the device build of the augmented design (rows in input order)
+    const BuildIn in{N, pc, a_time, a_event, a_str, acp.data(), a_rows, a_vals, true};
+    return build_core(ctx, in, perm_out);
 }

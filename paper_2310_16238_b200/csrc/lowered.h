@@ -7,6 +7,24 @@
 #include <string>
 #include <vector>
 
+#include "../../include/stratcox_b200.h"
+
+
+// One output column of the lowering: source covariate, effect window (-1 =
+// unsplit) and its [start, end) (transforms.cpp:98-175).
+struct LowerCol {
+    int64_t src;
+    int window;
+    double start, end;
+};
+
+// Validation (cut points, follow-up coverage, subject times, split spec) and
+// the output columns; false with the reference's message on failure.
+bool lowering_plan(const scx_dataset* subjects, const double* cut_points, int64_t n_cuts,
+                   const int64_t* split_covariate, const int64_t* split_ptr,
+                   const double* split_times, int64_t n_splits, std::vector<LowerCol>& cols,
+                   std::string& err);
+
 struct scx_lowered {
     std::vector<double> time;
     std::vector<uint8_t> event;

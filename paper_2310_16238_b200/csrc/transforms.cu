@@ -58,21 +58,12 @@ std::string short_number(double v) {
 
 }  // namespace
 
-extern "C" {
-
-scx_status scx_lower_time_varying(const scx_dataset* subj, const double* cut_points, int64_t n_cuts,
-                                  const int64_t* split_covariate, const int64_t* split_ptr,
-                                  const double* split_times, int64_t n_splits, scx_lowered** out,
-                                  char* error_out, int error_cap) {
-    auto report = [&](const std::string& m) {
-        if (error_out && error_cap > 0) {
-            std::strncpy(error_out, m.c_str(), (size_t)error_cap - 1);
-            error_out[error_cap - 1] = 0;
-        }
-        return SCX_ERR_VALIDATION;
-    };
-    if (!subj || !cut_points || !out) return report("null argument");
-    *out = nullptr;
+// Validation and output-column plan of the lowering (transforms.cpp:39-175 and
+// make_time_varying's coverage check), shared with the device lowering.
+bool lowering_plan(const scx_dataset* subj, const double* cut_points, int64_t n_cuts,
+                   const int64_t* split_covariate, const int64_t* split_ptr,
+                   const double* split_times, int64_t n_splits, std::vector<LowerCol>& cols,
+                   std::string& err) {
     try {
         const std::vector<double> cuts(cut_points, cut_points + n_cuts);
         // validate_cut_points (transforms.cpp:39-46)
@@ -82,17 +73,13 @@ scx_status scx_lower_time_varying(const scx_dataset* subj, const double* cut_poi
             if (!std::isfinite(cuts[i]) || cuts[i] <= cuts[i - 1])
                 throw LowerError("cut points must be finite and strictly increasing");
         const int64_t n = subj->n_rows, p = subj->n_covariates;
-        const int k_count = (int)cuts.size() - 1;
-        std::vector<int64_t> subject(n);
-        for (int64_t i = 0; i < n; ++i) subject[i] = subj->subject ? subj->subject[i] : i + 1;
         for (int64_t i = 0; i < n; ++i)  // make_time_varying (:74-79)
             if (subj->time[i] > cuts.back())
                 throw LowerError("cut points do not cover follow-up of subject " +
-                                 std::to_string(subject[i]));
+                                 std::to_string(subj->subject ? subj->subject[i] : i + 1));
         for (int64_t i = 0; i < n; ++i)  // validate (:48-62)
             if (!std::isfinite(subj->time[i]) || subj->time[i] < 0.0)
                 throw LowerError("negative or non-finite time for subject index " + std::to_string(i));
-
         // split_time_varying_coefficient (:98-175): effect-window edges per covariate
         std::vector<std::vector<double>> bounds(p);
         for (int64_t sidx = 0; sidx < n_splits; ++sidx) {
@@ -113,14 +100,7 @@ scx_status scx_lower_time_varying(const scx_dataset* subj, const double* cut_poi
             }
             bounds[j].assign(seen.begin(), seen.end());
         }
-        auto* L = new scx_lowered();
-        // output columns: per source covariate, one column or one per window
-        struct OutCol {
-            int64_t src;
-            int window;
-            double start, end;
-        };
-        std::vector<OutCol> cols;
+        cols.clear();
         for (int64_t j = 0; j < p; ++j) {
             if (bounds[j].empty()) {
                 cols.push_back({j, -1, cuts.front(), cuts.back()});
@@ -131,6 +111,47 @@ scx_status scx_lower_time_varying(const scx_dataset* subj, const double* cut_poi
             edges.push_back(cuts.back());
             for (size_t w = 0; w + 1 < edges.size(); ++w) cols.push_back({j, (int)w, edges[w], edges[w + 1]});
         }
+        return true;
+    } catch (const LowerError& e) {
+        err = e.what();
+        return false;
+    }
+}
+
+extern "C" {
+
+scx_status scx_lower_time_varying(const scx_dataset* subj, const double* cut_points, int64_t n_cuts,
+                                  const int64_t* split_covariate, const int64_t* split_ptr,
+                                  const double* split_times, int64_t n_splits, scx_lowered** out,
+                                  char* error_out, int error_cap) {
+    auto report = [&](const std::string& m) {
+        if (error_out && error_cap > 0) {
+            std::strncpy(error_out, m.c_str(), (size_t)error_cap - 1);
+            error_out[error_cap - 1] = 0;
+        }
+        return SCX_ERR_VALIDATION;
+    };
+    if (!subj || !cut_points || !out) return report("null argument");
+    *out = nullptr;
+    try {
+        const std::vector<double> cuts(cut_points, cut_points + n_cuts);
+        std::vector<LowerCol> plan;
+        std::string why;
+        if (!lowering_plan(subj, cut_points, n_cuts, split_covariate, split_ptr, split_times, n_splits,
+                           plan, why))
+            throw LowerError(why);
+        const int64_t n = subj->n_rows;
+        const int k_count = (int)cuts.size() - 1;
+        std::vector<int64_t> subject(n);
+        for (int64_t i = 0; i < n; ++i) subject[i] = subj->subject ? subj->subject[i] : i + 1;
+        auto* L = new scx_lowered();
+        struct OutCol {
+            int64_t src;
+            int window;
+            double start, end;
+        };
+        std::vector<OutCol> cols;
+        for (const LowerCol& c : plan) cols.push_back({c.src, c.window, c.start, c.end});
         // augment_to_strata (:177-223): interval-major rows, subjects in input
         // order; rank[k-1][i] = augmented row of subject i in interval k (-1: not at risk)
         std::vector<std::vector<int64_t>> rank(k_count, std::vector<int64_t>(n, -1));

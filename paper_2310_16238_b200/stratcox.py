@@ -660,6 +660,46 @@ def build_design(data: SurvivalDataset, device: int = 0):
     return dd, perm
 
 
+def build_lowered_design(subjects: SurvivalDataset, cut_points, splits=None, device: int = 0):
+    """Device lowering + build (scx_build_lowered_design): only the subject-level
+    data is uploaded; augment_to_strata / split_time_varying_coefficient and
+    build_sorted_design run on the GPU. Returns (DeviceDesign, perm,
+    [ColumnMapEntry]) — the design lower_time_varying + build_design give."""
+    lib = _lib()
+    splits = splits or {}
+    cov = np.array(sorted(splits), np.int64)
+    sptr = np.zeros(len(cov) + 1, np.int64)
+    times: List[float] = []
+    for q, j in enumerate(cov):
+        times += [float(t) for t in splits[int(j)]]
+        sptr[q + 1] = len(times)
+    tm = np.array(times, np.float64)
+    cuts = np.ascontiguousarray(cut_points, np.float64)
+    pout = subjects.n_covariates() + len(times)
+    src = np.empty(max(pout, 1), np.int64); win = np.empty(max(pout, 1), np.int32)
+    ws = np.empty(max(pout, 1)); we = np.empty(max(pout, 1))
+    h = C.c_void_p()
+    if lib.scx_create(int(device), C.byref(h)) != 0:
+        raise CudaError(f"scx_create(device={device}) failed: no usable sm_100 device")
+    ds, keep = subjects._c()
+    rc = lib.scx_build_lowered_design(h, C.byref(ds), ptr(cuts, C.c_double), cuts.shape[0],
+                                      ptr(cov, C.c_int64), ptr(sptr, C.c_int64),
+                                      ptr(tm, C.c_double), len(cov), None, ptr(src, C.c_int64),
+                                      win.ctypes.data_as(C.POINTER(C.c_int32)),
+                                      ptr(ws, C.c_double), ptr(we, C.c_double))
+    if rc != 0:
+        msg = lib.scx_last_error(h).decode()
+        lib.scx_destroy(h)
+        raise _ERR.get(rc, StratcoxError)(msg)
+    dd = DeviceDesign.__new__(DeviceDesign)
+    dd._h, dd.device, dd._state_owner = h, device, None
+    info = dd.info()
+    dd.design = _BuiltDesign(info["n_rows"], info["n_strata"], info["p"])
+    cmap = [ColumnMapEntry(c, int(src[c]), int(win[c]), float(ws[c]), float(we[c]))
+            for c in range(pout)]
+    return dd, cmap
+
+
 def fold_assignment(data: SurvivalDataset, folds: int, seed: int) -> np.ndarray:
     """fold_assignment (resample.hpp:45, resample.cpp:70-91)."""
     ds, keep = data._c()

@@ -1,2 +1,3 @@
-free -g > gpurun_out/free.txt; nproc >> gpurun_out/free.txt
-timeout 1500 python scripts/parity_c4_full.py > gpurun_out/parity_full.log 2>&1; echo "rc=$?" >> gpurun_out/parity_full.log
+timeout 600 python bench.py --config c2 > gpurun_out/bench_c2.log 2>&1
+timeout 600 python bench.py --config c3 > gpurun_out/bench_c3.log 2>&1
+timeout 600 python bench.py --config c1 > gpurun_out/bench_c1.log 2>&1

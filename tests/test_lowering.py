@@ -75,3 +75,41 @@ def test_fit_on_lowered_design_matches_oracle(ref, oracle):
     assert r.cycles_used == want["cycles"]
     assert np.max(np.abs(r.beta - want["beta"])) <= 1e-8
     assert np.allclose(r.objective_trace, want["trace"], rtol=1e-10, atol=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p,seed,cuts,splits,values", [
+    (500, 4, 2, [0, 1, 2.5, 4, 8], {1: [2.5], 3: [1, 4]}, False),
+    (3000, 5, 4, list(np.linspace(0, 8, 21)), {0: list(np.linspace(0, 8, 21)[1:-1]), 2: [4.0]}, True),
+    (200000, 6, 6, list(np.linspace(0, 20, 21)), {0: list(np.linspace(0, 20, 21)[1:-1])}, False),
+])
+def test_device_lowering_matches_reference(ref, n, p, seed, cuts, splits, values):
+    """scx_build_lowered_design (subjects uploaded, augmentation + build on the
+    device) gives the reference's lower_pipeline + build_sorted_design: perm,
+    offsets, tie ends, rows and values bit for bit, and the column map."""
+    from oracle.oracle_py import Dataset
+    ds = ref.random_dataset(seed, n, 1, p, 0.3, 8 if n < 10000 else 20)
+    subj = np.arange(n, dtype=np.int64) * 3 + 7
+    if values:
+        ds = Dataset(ds.time, ds.event, ds.stratum, ds.col_ptr, ds.row_idx,
+                     np.round(ds.values * 3) / 2)  # some zero values: never stored
+    low, wsubj, wsrc, wwin = ref.lower_pipeline(ds, cuts, splits, subject=subj)
+    h, a = ref.build_design(low)
+    ref.free_design(h)
+    dd, cmap = sx.build_lowered_design(_sx(ds, subj), cuts, splits)
+    e = dd.export()
+    dd.close()
+    assert [c.source for c in cmap] == wsrc.tolist() and [c.window for c in cmap] == wwin.tolist()
+    for k in ("offsets", "event", "tie_end", "col_ptr", "row_idx"):
+        assert np.array_equal(e[k], a[k]), k
+    assert np.array_equal(e["values"], a["values"])
+
+
+@pytest.mark.gpu
+def test_device_lowering_validation_messages(ref):
+    ds = _subjects_dataset(ref, 50, 2, 9, 8)
+    for cuts, splits, msg in [([1, 8], None, "first cut point must be 0"),
+                              ([0, 4], None, "cut points do not cover follow-up"),
+                              ([0, 4, 8], {0: [3]}, "is not a cut point")]:
+        with pytest.raises(sx.ValidationError, match=msg):
+            sx.build_lowered_design(_sx(ds), cuts, splits)
