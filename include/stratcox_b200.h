@@ -371,6 +371,12 @@ scx_status scx_set_k1_mode(scx_ctx* ctx, int mode, int* chunked);
  * with SCX_K1_DBG bit 8 set (CTAs 0 and 73, tiles < 511): out[2][512][8]. */
 scx_status scx_debug_k1_trace(long long* out);
 
+/* Debug: the risk scan's arrays after scx_risk_prefix — tile-local suffix sums
+ * R[n], Q[n], tile carries CR / CQ [2048-row tiles] and each tile's last-head
+ * offset; R of row r = R[r] + (r mod 2048 >= lasth[r / 2048] ? CR[r / 2048] : 0). */
+scx_status scx_debug_risk_arrays(scx_ctx* ctx, double* R, double* Q, double* CR, double* CQ,
+                                 int32_t* lasth);
+
 /* Number of kernels this context has launched so far (bench bookkeeping). */
 int64_t scx_launch_count(const scx_ctx* ctx);
 

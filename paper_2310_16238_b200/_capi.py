@@ -91,6 +91,7 @@ SIGNATURES = {
     "scx_launch_count": (C.c_int64, [_vp]),
     "scx_debug_k1_trace": (C.c_int, [_i64p]),
     "scx_set_k1_mode": (C.c_int, [_vp, C.c_int, _ip]),
+    "scx_debug_risk_arrays": (C.c_int, [_vp, _dp, _dp, _dp, _dp, C.POINTER(C.c_int32)]),
     "scx_set_sm_budget": (C.c_int, [_vp, C.c_int]),
     "scx_xchg_slots": (C.c_int, [_vp, C.POINTER(C.c_void_p)]),
     "scx_xchg_ipc_handle": (C.c_int, [_vp, C.c_char_p]),

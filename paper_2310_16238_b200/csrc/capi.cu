@@ -145,7 +145,7 @@ void free_design(scx_ctx* ctx) {
                     ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
                     ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, d.lasth1, d.ref_act,
                     d.ref_abeg, d.ref_avo, d.ref_ab, d.ref_nact, d.ref_meta,
-                    d.chunk_rows, ctx->cols_d, d.rs_u, d.rs_R, d.rs_Q, d.chunk_k, ctx->col1_d};
+                    d.chunk_rows, ctx->cols_d, d.rs_CR, d.rs_CQ, d.rs_R, d.rs_Q, d.chunk_k, ctx->col1_d};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     const DevCtl* keep_ctl = d.ctl;
@@ -740,16 +740,24 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
             std::vector<int32_t> ck(ch.size());
             int32_t q = 0;
             int32_t most = 0;
+            int64_t most_tiles = 0;  // 2048-row tiles a chunk touches (risk-scan tile carries)
             for (size_t c = 0; c < ch.size(); ++c) {
                 while (q < k && offsets[q] < ch[c]) ++q;
                 ck[c] = q;
-                if (c > 0) most = std::max(most, ck[c] - ck[c - 1]);
+                if (c > 0) {
+                    most = std::max(most, ck[c] - ck[c - 1]);
+                    most_tiles = std::max<int64_t>(
+                        most_tiles, (ch[c] - 1) / kK1TileRows - ch[c - 1] / kK1TileRows + 1);
+                }
             }
-            if (most <= kRsMaxStrata) {
+            if (most <= kRsMaxStrata && most_tiles <= kRsTileInfo) {
                 CK(dmalloc(&d.chunk_k, ck.size()));
                 CK(cudaMemcpyAsync(d.chunk_k, ck.data(), ck.size() * sizeof(int32_t),
                                    cudaMemcpyHostToDevice, s));
-                CK(dmalloc(&d.rs_u, d.npad));
+                CK(dmalloc(&d.rs_CR, d.ntiles1));
+                CK(dmalloc(&d.rs_CQ, d.ntiles1));
+                CK(cudaMemsetAsync(d.rs_CR, 0, d.ntiles1 * sizeof(double), s));
+                CK(cudaMemsetAsync(d.rs_CQ, 0, d.ntiles1 * sizeof(double), s));
                 CK(dmalloc(&d.rs_R, d.npad));
                 CK(dmalloc(&d.rs_Q, d.npad));
                 d.rs_ok = 1;
@@ -775,7 +783,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     d.offsets = ctx->offsets_d;
     if (!make_tmap(&d.tmap_D, d.D, d.npad) || !make_tmap(&d.tmap_eta, d.eta, d.npad) ||
         !make_tmap(&d.tmap_D1, d.D, d.npad, kK1TileRows) ||
-        (d.rs_ok && (!make_tmap(&d.tmap_u, d.rs_u, d.npad, kK1TileRows) || !make_tmap(&d.tmap_R, d.rs_R, d.npad, kK1TileRows) ||
+        (d.rs_ok && (!make_tmap(&d.tmap_R, d.rs_R, d.npad, kK1TileRows) ||
                      !make_tmap(&d.tmap_Q, d.rs_Q, d.npad, kK1TileRows))))
         return fail(ctx, SCX_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 
@@ -1035,6 +1043,22 @@ scx_status scx_risk_prefix(scx_ctx* ctx) {
     tmark(ctx, 3);
     KL(1, launch_rs_cycle(ctx->d, ctx->cols_d, 0, 2, ctx->stream));
     tend(ctx);
+    return SCX_OK;
+}
+
+scx_status scx_debug_risk_arrays(scx_ctx* ctx, double* R, double* Q, double* CR, double* CQ,
+                                 int32_t* lasth) {
+    if (scx_status s = need_design(ctx)) return s;
+    if (!ctx->d.rs_ok) return fail(ctx, SCX_ERR_VALIDATION, "no risk-suffix layout");
+    cudaSetDevice(ctx->device);
+    const DesignDev& d = ctx->d;
+    cudaStream_t s = ctx->stream;
+    if (R) CK(cudaMemcpyAsync(R, d.rs_R, d.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (Q) CK(cudaMemcpyAsync(Q, d.rs_Q, d.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (CR) CK(cudaMemcpyAsync(CR, d.rs_CR, d.ntiles1 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (CQ) CK(cudaMemcpyAsync(CQ, d.rs_CQ, d.ntiles1 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (lasth) CK(cudaMemcpyAsync(lasth, d.lasth1, d.ntiles1 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     return SCX_OK;
 }
 

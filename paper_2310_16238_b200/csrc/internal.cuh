@@ -118,6 +118,7 @@ enum RsStop : int {
 constexpr double kRsEtaBound = 300.0;  // w/S0^2 and a*Q*(a+2C) stay in fp64 range below it
 constexpr int kWarnCap = 1 << 16;     // warnings recorded per fit (the count is exact)
 constexpr int kRsMaxStrata = 1024;     // strata of one chunk staged in shared memory
+constexpr int kRsTileInfo = 512;       // 2048-row tiles of one chunk (risk-scan tile carries)
 
 struct Pref1 {
     double v0;
@@ -276,7 +277,9 @@ __device__ __forceinline__ bool xchg_values(const Xchg& x, unsigned long long k,
     const int s = (int)(k & 1ull);
     if (publish) {
         XSlot* own = x.slot[x.rank] + s;
-        for (int i = 0; i < n; ++i) own->v[i] = mine[i];
+#pragma unroll
+        for (int i = 0; i < kXVals; ++i)  // unrolled with a guard: mine[] stays in registers
+            if (i < n) own->v[i] = mine[i];
         own->err = err_mine;
         __threadfence_system();
         *((volatile unsigned long long*)&own->seq) = k + 1;
@@ -291,10 +294,11 @@ __device__ __forceinline__ bool xchg_values(const Xchg& x, unsigned long long k,
     }
     __threadfence_system();
     int e = 0;
-    for (int i = 0; i < n; ++i) out[i] = op ? 0.0 : 0.0;
     for (int r = 0; r < x.nranks; ++r) {
         const XSlot* ps = x.slot[r] + s;
-        for (int i = 0; i < n; ++i) {
+#pragma unroll
+        for (int i = 0; i < kXVals; ++i) {
+            if (i >= n) continue;
             const double v = __ldcv(&ps->v[i]);
             out[i] = op ? (r == 0 ? v : fmax(out[i], v)) : (r == 0 ? v : out[i] + v);
         }
@@ -351,10 +355,10 @@ struct DesignDev {
     int coop_blocks;          // co-resident blocks for the cooperative kernels
     int sm_budget;            // SMs of a rank sharing the GPU (0: all)
     // risk-suffix CCD cycle (chunk layout only)
-    double* rs_u;             // [npad] scratch: w/S0 per row (forward pass)
+    double* rs_CR;            // [ntiles1] risk scan: carry of each tile's open segment (R)
+    double* rs_CQ;            // [ntiles1] ... (Q)
     double* rs_R;             // [npad] within-stratum suffix sum of w/S0 from each row
     double* rs_Q;             // [npad] within-stratum suffix sum of w/S0^2 from each row
-    CUtensorMap tmap_u;       // box 16 x 256 (4096-row tile), loads and stores
     CUtensorMap tmap_R;
     CUtensorMap tmap_Q;
     int32_t* chunk_k;         // [nchunks+1] first stratum of each chunk
