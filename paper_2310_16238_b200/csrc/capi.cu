@@ -145,7 +145,8 @@ void free_design(scx_ctx* ctx) {
                     ctx->col_beg_d, ctx->val_off_d, ctx->offsets_d, ctx->rows_d,
                     ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, d.lasth1, d.ref_act,
                     d.ref_abeg, d.ref_avo, d.ref_ab, d.ref_nact, d.ref_meta,
-                    d.chunk_rows, ctx->cols_d, d.rs_CR, d.rs_CQ, d.rs_R, d.rs_Q, d.chunk_k, ctx->col1_d};
+                    d.chunk_rows, ctx->cols_d, d.rs_CR, d.rs_CQ, d.rs_R, d.rs_Q, d.chunk_k, ctx->col1_d,
+                    d.ell_col, d.ell_val, d.ell_base};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     const DevCtl* keep_ctl = d.ctl;
@@ -834,6 +835,17 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     if (!ctx->zero_cols.empty())
         CK(cudaMemcpyAsync(ctx->zero_cols_d, ctx->zero_cols.data(),
                            ctx->zero_cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    // row-slice copy of the design for the 256-update refresh (skipped, and
+    // the tile refresh kept, when the re-sort's scratch does not fit)
+    {
+        cudaError_t e = build_refresh_ell(d, nnz, n_ind < p, s);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            d.ell_ok = 0;
+        } else {
+            CK(e);
+        }
+    }
     ctx->nnz = nnz;
     ctx->n_indicator = n_ind;
     ctx->has_design = true;
@@ -843,7 +855,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         return st;
     }
     // state at beta = 0 (make_state)
-    KL(kRefreshLaunches, launch_refresh(d, s));
+    KL(refresh_launches(d), launch_refresh(d, s));
     return check_device_error(ctx);
 }
 
@@ -938,7 +950,7 @@ scx_status scx_make_state(scx_ctx* ctx, const double* beta) {
     cudaSetDevice(ctx->device);
     DesignDev& d = ctx->d;
     if (d.p > 0) CK(cudaMemcpyAsync(d.beta, beta, d.p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    KL(kRefreshLaunches, launch_refresh(d, ctx->stream));
+    KL(refresh_launches(d), launch_refresh(d, ctx->stream));
     return check_device_error(ctx);
 }
 
@@ -981,7 +993,7 @@ scx_status scx_get_state(scx_ctx* ctx, double* beta, double* xbeta, double* exp_
 scx_status scx_refresh_xbeta(scx_ctx* ctx) {
     if (scx_status s = need_design(ctx)) return s;
     cudaSetDevice(ctx->device);
-    KL(kRefreshLaunches, launch_refresh(ctx->d, ctx->stream));
+    KL(refresh_launches(ctx->d), launch_refresh(ctx->d, ctx->stream));
     return check_device_error(ctx);
 }
 
@@ -1269,7 +1281,7 @@ static scx_status fused_cycle(scx_ctx* ctx, const ColArgs* cols, int32_t n, bool
     if (resumed) *resumed = r;
     if (r > 0) {
         // 256 accepted updates: refresh eta/D from beta, then resume
-        KL(kRefreshLaunches, launch_refresh(d, s));
+        KL(refresh_launches(d), launch_refresh(d, s));
         if (scx_status st = check_device_error(ctx)) return st;
     }
     return SCX_OK;
@@ -1366,7 +1378,7 @@ scx_status scx_ccd_fit_prior(scx_ctx* ctx, const double* gamma, const double* l2
         CK(cudaMemcpyAsync(&c->hmax, &izero, sizeof izero, cudaMemcpyHostToDevice, s));
     }
     // make_state (likelihood.cpp:19-29)
-    KL(kRefreshLaunches, launch_refresh(d, s));
+    KL(refresh_launches(d), launch_refresh(d, s));
     if (scx_status st = check_device_error(ctx)) return st;
 
     double ll, pen, max_step;
@@ -1400,7 +1412,7 @@ scx_status scx_ccd_fit_prior(scx_ctx* ctx, const double* gamma, const double* l2
                         const int why = ctx->ctl_h->rs_reason;
                         if (why == kRsDone) break;
                         if (why == kRsRefresh) {
-                            KL(kRefreshLaunches, launch_refresh(d, s));
+                            KL(refresh_launches(d), launch_refresh(d, s));
                             if (sharded) KL(1, launch_xchg_ctl(d, 0, s));  // global max|eta|
                             if (scx_status st = check_device_error(ctx)) return st;
                         } else if (why == kRsBound) {

@@ -659,6 +659,78 @@ __global__ void __launch_bounds__(256) k_lw_fill(const LwCol* cols, const int64_
     }
 }
 
+// ---------------------------------------------------------------- refresh layout (row slices)
+// The 256-update refresh (likelihood.cpp:31-58) as a row-parallel pass: the
+// design's entries re-sorted by row (stable, so a row's entries keep the
+// ascending column order) and laid out in 32-row slices, so a warp reads 32
+// rows' next entries with coalesced loads and every lane folds its own row in
+// the reference's column order, without any synchronisation (k_refresh_ell in
+// kernels.cu).
+// Within a slice, entries come in groups of 4 per row: entry k of row l at
+// base[s] + 128*(k/4) + 4l + k%4 (row lengths padded to a multiple of 4).
+__global__ void k_iota_u32(uint32_t* v, int64_t m) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (uint32_t)i;
+}
+// first sorted entry of each row (keys sorted ascending), rowptr[n] = nnz
+__global__ void k_row_starts(const uint32_t* keys, int64_t nnz, int64_t n, int64_t* rowptr) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < (uint32_t)r)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        rowptr[r] = lo;
+    }
+}
+// slice widths: max row length of each 32-row slice
+__global__ void k_slice_width(const int64_t* rowptr, int64_t n, int64_t nsl, int32_t* width) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nsl) return;
+    const int64_t r = w * 32 + lane;
+    int len = r < n ? (int)(rowptr[r + 1] - rowptr[r]) : 0;
+    for (int o = 16; o; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+    if (lane == 0) width[w] = len;
+}
+template <typename IdT>
+__global__ void k_fill_ids(IdT* v, int64_t m, IdT x) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = x;
+}
+template <typename IdT>
+__global__ void k_ell_fill(const uint32_t* keys, const uint32_t* ent, int64_t nnz,
+                           const int64_t* rowptr, const int64_t* base, const int64_t* col_beg,
+                           int64_t p, const int64_t* val_off, const double* vals, IdT* ell_col,
+                           double* ell_val) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = keys[i];
+        const int64_t e = ent[i];
+        int64_t lo = 0, hi = p;  // the column of entry e: col_beg[c] <= e < col_beg[c + 1]
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (col_beg[mid] <= e)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const int64_t k = i - rowptr[r];
+        const int64_t pos = base[r >> 5] + (k >> 2) * 128 + (int64_t)(r & 31) * 4 + (k & 3);
+        ell_col[pos] = (IdT)lo;
+        if (ell_val) {
+            const int64_t vo = val_off[lo];
+            ell_val[pos] = vo < 0 ? 1.0 : vals[vo + (e - col_beg[lo])];
+        }
+    }
+}
+
 }  // namespace scx
 
 // ---------------------------------------------------------------- host driver
@@ -1118,4 +1190,96 @@ extern "C" scx_status scx_build_lowered_design(scx_ctx* ctx, const scx_dataset* 
     // ... and the device build of the augmented design (rows in input order)
     const BuildIn in{N, pc, a_time, a_event, a_str, acp.data(), a_rows, a_vals, true};
     return build_core(ctx, in, perm_out);
+}
+
+
+// ---------------------------------------------------------------- refresh layout builder
+// Called at upload (capi.cu). Leaves d.ell_ok = 0 (the tile refresh stays in
+// use) when the design is too large for the re-sort's scratch.
+cudaError_t scx::build_refresh_ell(DesignDev& d, int64_t nnz, bool any_values, cudaStream_t s) {
+    d.ell_ok = 0;
+    const int64_t n = d.n, p = d.p;
+    if (nnz <= 0 || p <= 0 || nnz >= ((int64_t)1 << 32)) return cudaSuccess;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t need = (size_t)nnz * (16 + 2 * 4 + (any_values ? 10 : 3)) + (size_t)n * 16;
+    if (need > free_b / 2) return cudaSuccess;  // leave room for the fit's own scratch
+    DevBuf B;
+    uint32_t *keys, *keys2, *ent, *ent2;
+    if (B.alloc(&keys, nnz) || B.alloc(&keys2, nnz) || B.alloc(&ent, nnz) || B.alloc(&ent2, nnz))
+        return cudaGetLastError();
+    cudaMemcpyAsync(keys, d.rows, nnz * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+    k_iota_u32<<<grid_sms((nnz + 255) / 256), 256, 0, s>>>(ent, nnz);
+    // stable radix by row (one segment): column order kept inside a row
+    TileMap tm;
+    std::vector<int64_t> tb_h, st0_h;
+    std::vector<int32_t> tseg_h;
+    make_tiles({0, nnz}, tb_h, tseg_h, st0_h);
+    tm.ntiles = (int64_t)tseg_h.size();
+    tm.nseg = 1;
+    uint32_t *hist, *segtot;
+    int64_t zero = 0;
+    if (B.alloc(&hist, tm.ntiles * 256) || B.alloc(&segtot, 256) || B.alloc(&tm.tb, tm.ntiles + 1) ||
+        B.alloc(&tm.tseg, tm.ntiles) || B.alloc(&tm.st0, 2) || B.alloc(&tm.sbeg, 1))
+        return cudaGetLastError();
+    cudaMemcpyAsync(tm.tb, tb_h.data(), (tm.ntiles + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(tm.tseg, tseg_h.data(), tm.ntiles * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(tm.st0, st0_h.data(), 2 * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(tm.sbeg, &zero, sizeof zero, cudaMemcpyHostToDevice, s);
+    uint64_t varying = 0;
+    for (int64_t v = n - 1; v > 0; v >>= 1) varying = (varying << 1) | 1;
+    if (cudaError_t e = radix_sort<uint32_t>(keys, keys2, ent, ent2, true, tm, varying, hist, segtot, s))
+        return e;
+    int64_t* rowptr;
+    const int64_t nsl = (n + 31) / 32;
+    int32_t* width_d;
+    if (B.alloc(&rowptr, n + 1) || B.alloc(&width_d, nsl)) return cudaGetLastError();
+    k_row_starts<<<grid_sms((n + 256) / 256), 256, 0, s>>>(keys, nnz, n, rowptr);
+    k_slice_width<<<(unsigned)((nsl * 32 + 255) / 256), 256, 0, s>>>(rowptr, n, nsl, width_d);
+    std::vector<int32_t> width(nsl);
+    cudaMemcpyAsync(width.data(), width_d, nsl * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (cudaError_t e = cudaStreamSynchronize(s)) return e;
+    std::vector<int64_t> base(nsl + 1, 0);
+    for (int64_t w = 0; w < nsl; ++w) base[w + 1] = base[w] + 32 * (((int64_t)width[w] + 3) & ~3LL);
+    const int64_t cells = base[nsl];
+    const bool wide = p >= 65535;  // u16 ids 0..p-1 plus the padding id p
+    void* col = nullptr;
+    double* val = nullptr;
+    int64_t* base_d = nullptr;
+    if (cudaMalloc(&col, std::max<int64_t>(cells, 1) * (wide ? 4 : 2)) != cudaSuccess) return cudaGetLastError();
+    if (any_values && cudaMalloc((void**)&val, std::max<int64_t>(cells, 1) * sizeof(double)) != cudaSuccess) {
+        cudaFree(col);
+        return cudaGetLastError();
+    }
+    if (cudaMalloc((void**)&base_d, (nsl + 1) * sizeof(int64_t)) != cudaSuccess) {
+        cudaFree(col);
+        cudaFree(val);
+        return cudaGetLastError();
+    }
+    // padding: column id p (beta_p reads as 0 in the refresh)
+    if (wide)
+        k_fill_ids<uint32_t><<<grid_sms((cells + 255) / 256), 256, 0, s>>>(static_cast<uint32_t*>(col), cells, (uint32_t)p);
+    else
+        k_fill_ids<uint16_t><<<grid_sms((cells + 255) / 256), 256, 0, s>>>(static_cast<uint16_t*>(col), cells, (uint16_t)p);
+    cudaMemcpyAsync(base_d, base.data(), (nsl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    const int g = grid_sms((nnz + 255) / 256);
+    if (wide)
+        k_ell_fill<uint32_t><<<g, 256, 0, s>>>(keys, ent, nnz, rowptr, base_d, d.col_beg, p, d.val_off,
+                                               d.vals, static_cast<uint32_t*>(col), val);
+    else
+        k_ell_fill<uint16_t><<<g, 256, 0, s>>>(keys, ent, nnz, rowptr, base_d, d.col_beg, p, d.val_off,
+                                               d.vals, static_cast<uint16_t*>(col), val);
+    if (cudaError_t e = cudaStreamSynchronize(s)) {
+        cudaFree(col);
+        cudaFree(val);
+        cudaFree(base_d);
+        return e;
+    }
+    d.ell_col = col;
+    d.ell_val = val;
+    d.ell_base = base_d;
+    d.ell_nsl = nsl;
+    d.ell_wide = wide ? 1 : 0;
+    d.ell_ok = 1;
+    return cudaSuccess;
 }

@@ -344,6 +344,14 @@ struct DesignDev {
     int32_t* ref_nact;        // [1] number of active columns
     int32_t* ref_meta;        // [ntiles1+1][ref_ps] tptr of the active columns, transposed
     int64_t ref_ps;           // row stride of ref_meta (p rounded up to 32)
+    // refresh in row slices (build_refresh_ell): entry k of row 32s+l at
+    // ell_base[s] + 128(k/4) + 4l + k%4; column ids u16 (u32 when ell_wide), p = padding
+    void* ell_col;
+    double* ell_val;          // NULL: every value 1.0
+    int64_t* ell_base;        // [ell_nsl + 1]
+    int64_t ell_nsl;
+    int32_t ell_wide;
+    int32_t ell_ok;           // the row-slice refresh is available
     // look-back scratch
     unsigned int* status;     // [ntiles]
     double* slots;            // [2][ntiles][4] agg / inc (s0, s1, s2, flag)
@@ -385,7 +393,9 @@ cudaError_t launch_k3(const DesignDev& d, const ColArgs& col, int mode, double d
                       cudaStream_t s);
 // refresh eta/D from beta (make_state / refresh_xbeta)
 // kernels launched by launch_refresh (active columns, their tile table, the tiles, finish)
+// (2 when the row-slice refresh runs: the slices, finish)
 constexpr int kRefreshLaunches = 4;
+int refresh_launches(const DesignDev& d);
 cudaError_t launch_refresh(const DesignDev& d, cudaStream_t s);
 cudaError_t launch_naive_gh(const DesignDev& d, const ColArgs& col, double* xdense,
                             double* out2, cudaStream_t s);
@@ -394,6 +404,7 @@ cudaError_t launch_zero_cols(const DesignDev& d, const int32_t* cols, int64_t nc
 // multi-GPU: rank-summed partials + rule (k_shard_step); ctl exchanges
 // (what 0: max mbound, 1: sum ll + max mbound, 2: max halving level)
 void preload_sharded_kernels(const DesignDev& d);
+cudaError_t build_refresh_ell(DesignDev& d, int64_t nnz, bool any_values, cudaStream_t s);
 cudaError_t launch_shard_step(const DesignDev& d, const ColArgs& col, cudaStream_t s);
 cudaError_t launch_xchg_ctl(const DesignDev& d, int what, cudaStream_t s);
 // design preparation

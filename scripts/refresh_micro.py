@@ -3,8 +3,11 @@ with the end-of-fit active set (about 19% of the columns nonzero).
 
 python scripts/refresh_micro.py [--n 1e7] [--p 10000] [--active 0.19] [--reps 10]
 Prints the per-call device time (CUDA events on the library stream, L2
-flushed before each call) and the algorithmic bytes/s: 4 B (row index) per
-entry of an active column + 16 B per row (eta, D written).
+flushed before each call) and the bytes/s of the column-tile refresh's
+algorithmic traffic: 4 B (row index) per entry of an active column + 16 B per
+row (eta, D written). The row-slice refresh (default when its copy of the
+design was built; SCX_REFRESH_ELL=0 selects the tile refresh) reads every
+entry's 2-B column id instead, whatever the active set.
 """
 import argparse
 import json
