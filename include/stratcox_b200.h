@@ -117,6 +117,10 @@ scx_status scx_gradient_hessian(scx_ctx* ctx, int64_t j, double* gradient, doubl
 scx_status scx_gradient_hessian_rs(scx_ctx* ctx, int64_t j, double* gradient, double* hessian);
 /* The risk-suffix fused scan alone over the current state (timing kind 3). */
 scx_status scx_risk_prefix(scx_ctx* ctx);
+/* reps back-to-back risk scans in ONE launch (timing kind 3): the scan's
+ * throughput as it runs inside the persistent fit kernel, without the launch
+ * and pipeline fill of a single scan. reps >= 1. */
+scx_status scx_risk_prefix_n(scx_ctx* ctx, int reps);
 /* CCD cycle implementation: 0 = automatic (risk-suffix cycle on the chunked
  * layout while max|eta| <= 300, the per-coordinate fused-scan cycle otherwise
  * and for coordinates whose g'' cancels), 1 = fused-scan cycle only.

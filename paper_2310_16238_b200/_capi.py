@@ -11,7 +11,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstratcox_b200.so")
+# SCX_LIB selects another build of the same library (the profiling build
+# libstratcox_b200_trace.so: make trace); default: the shipped one
+LIB_PATH = os.environ.get("SCX_LIB") or os.path.join(_HERE, "libstratcox_b200.so")
 
 _i8p = C.POINTER(C.c_uint8)
 _i32p = C.POINTER(C.c_int32)
@@ -64,6 +66,7 @@ SIGNATURES = {
     "scx_gradient_hessian": (C.c_int, [_vp, C.c_int64, _dp, _dp]),
     "scx_gradient_hessian_rs": (C.c_int, [_vp, C.c_int64, _dp, _dp]),
     "scx_risk_prefix": (C.c_int, [_vp]),
+    "scx_risk_prefix_n": (C.c_int, [_vp, C.c_int]),
     "scx_set_fit_path": (C.c_int, [_vp, C.c_int, _ip]),
     "scx_fit_path_stats": (C.c_int, [_vp, _i64p]),
     "scx_log_partial_likelihood": (C.c_int, [_vp, _dp]),
@@ -185,6 +188,8 @@ def load(path: str = LIB_PATH):
             "__graft_entry__.build()); there is no CPU fallback")
     lib = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("SCX_LIB") and not hasattr(lib, name):
+            continue  # an older profiling build (A/B): entry points it lacks stay unbound
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

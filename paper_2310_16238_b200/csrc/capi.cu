@@ -784,8 +784,8 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     d.offsets = ctx->offsets_d;
     if (!make_tmap(&d.tmap_D, d.D, d.npad) || !make_tmap(&d.tmap_eta, d.eta, d.npad) ||
         !make_tmap(&d.tmap_D1, d.D, d.npad, kK1TileRows) ||
-        (d.rs_ok && (!make_tmap(&d.tmap_R, d.rs_R, d.npad, kK1TileRows) ||
-                     !make_tmap(&d.tmap_Q, d.rs_Q, d.npad, kK1TileRows))))
+        (d.rs_ok && (!make_tmap(&d.tmap_R, d.rs_R, d.npad, kRsStoreRows) ||
+                     !make_tmap(&d.tmap_Q, d.rs_Q, d.npad, kRsStoreRows))))
         return fail(ctx, SCX_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 
     // co-resident block count for the cooperative kernels
@@ -1047,16 +1047,19 @@ scx_status scx_gradient_hessian_rs(scx_ctx* ctx, int64_t j, double* g, double* h
     return SCX_OK;
 }
 
-scx_status scx_risk_prefix(scx_ctx* ctx) {
+scx_status scx_risk_prefix_n(scx_ctx* ctx, int reps) {
     if (scx_status s = need_design(ctx)) return s;
     if (!ctx->d.rs_ok)
         return fail(ctx, SCX_ERR_VALIDATION, "risk-suffix evaluation needs the chunked layout");
+    if (reps < 1) return fail(ctx, SCX_ERR_VALIDATION, "reps must be >= 1");
     cudaSetDevice(ctx->device);
     tmark(ctx, 3);
-    KL(1, launch_rs_cycle(ctx->d, ctx->cols_d, 0, 2, ctx->stream));
+    KL(1, launch_rs_cycle(ctx->d, ctx->cols_d, reps, 2, ctx->stream));
     tend(ctx);
     return SCX_OK;
 }
+
+scx_status scx_risk_prefix(scx_ctx* ctx) { return scx_risk_prefix_n(ctx, 1); }
 
 scx_status scx_debug_risk_arrays(scx_ctx* ctx, double* R, double* Q, double* CR, double* CQ,
                                  int32_t* lasth) {
@@ -1527,7 +1530,7 @@ scx_status scx_timing_enable(scx_ctx* ctx, int on) {
 }
 scx_status scx_timing_reset(scx_ctx* ctx) {
     if (!ctx) return SCX_ERR_VALIDATION;
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 4; ++k) {  // every timing kind (0 fused scan .. 3 risk-suffix)
         ctx->timer.ms[k] = 0;
         ctx->timer.launches[k] = 0;
     }

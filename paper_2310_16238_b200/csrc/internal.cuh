@@ -118,7 +118,8 @@ enum RsStop : int {
 constexpr double kRsEtaBound = 300.0;  // w/S0^2 and a*Q*(a+2C) stay in fp64 range below it
 constexpr int kWarnCap = 1 << 16;     // warnings recorded per fit (the count is exact)
 constexpr int kRsMaxStrata = 1024;     // strata of one chunk staged in shared memory
-constexpr int kRsTileInfo = 512;       // 2048-row tiles of one chunk (risk-scan tile carries)
+constexpr int kRsTileInfo = 384;       // 2048-row tiles of one chunk (risk-scan tile carries)
+constexpr int kRsStoreRows = 512;      // rows of one risk-scan TMA store (one warp's rows)
 
 struct Pref1 {
     double v0;
@@ -379,7 +380,7 @@ enum K1Mode : int { kK1Eval = 0, kK1Fit = 1, kK1Diag = 2, kK1Partial = 3 };
 cudaError_t launch_k1(const DesignDev& d, const ColArgs& col, int mode, cudaStream_t s);
 cudaError_t k1_trace_copy(long long* out);
 // risk-suffix CCD cycle over cols_d[0..ncols): mode 0 fit, 1 evaluate cols_d[0]
-// only (g, h into ctl), 2 risk prefix only
+// only (g, h into ctl), 2 risk scan only (ncols back-to-back scans: throughput probe)
 cudaError_t launch_rs_cycle(const DesignDev& d, const ColArgs* cols_d, int ncols, int mode,
                             cudaStream_t s);
 // one CCD cycle in one cooperative launch over cols_d[0..ncols) (all of one

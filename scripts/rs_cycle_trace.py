@@ -15,6 +15,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["SCX_K1_DBG"] = "256"
+os.environ.setdefault("SCX_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2310_16238_b200", "libstratcox_b200_trace.so"))
 
 
 def main():
@@ -43,26 +44,23 @@ def main():
     n = int(np.max(np.nonzero(t[:, 0])[0])) + 1 if t[:, 0].any() else 0
     ph = {"grad_eval": 0, "grad_barrier_decide": 0, "full_eval": 0, "full_barrier_rule": 0,
           "apply": 0, "scan": 0}
+    cnt = {k: 0 for k in ph}
     nskip = 0
     for i in range(n):
         e = t[i]
         if not e[0]:
             continue
-        ph["grad_eval"] += e[1] - e[0] if e[1] else 0
-        ph["grad_barrier_decide"] += e[2] - e[1] if e[2] else 0
-        if e[3]:
-            ph["full_eval"] += e[3] - e[2]
-        if e[4]:
-            ph["full_barrier_rule"] += e[4] - e[3]
-        if e[5]:
-            ph["apply"] += e[5] - e[4]
-        if e[6]:
-            ph["scan"] += e[6] - e[5]
+        for key, a, b in (("grad_eval", 0, 1), ("grad_barrier_decide", 1, 2), ("full_eval", 2, 3),
+                          ("full_barrier_rule", 3, 4), ("apply", 4, 5), ("scan", 5, 6)):
+            if e[b] and e[a] and e[b] > e[a]:
+                ph[key] += e[b] - e[a]
+                cnt[key] += 1
         nskip += int(e[7])
     tot = int(t[n - 1][6] or t[n - 1][4] or t[n - 1][2]) - int(t[0][0])
     print(f"rounds={n} skipped={nskip} total_cycles={tot} ({tot / 1.965e3:.0f} us)")
     for k, v in ph.items():
-        print(f"  {k:22s} {int(v):>10d} cycles {int(v) / max(1, n):8.0f}/round  {v / max(1, tot):.1%}")
+        print(f"  {k:22s} {int(v):>10d} cycles {int(v) / max(1, n):8.0f}/round  {v / max(1, tot):.1%}"
+              f"  n={cnt[k]} {int(v) / max(1, cnt[k]) / 1.965e3:.1f} us each")
     print("stats", dd.fit_path_stats(), "cycles", r.cycles_used)
 
 

@@ -55,6 +55,18 @@ def main():
         ms = tot.value / max(1, nl.value)
         out[f"prefix_{mode}_us"] = ms * 1e3
         out[f"prefix_{mode}_gbs"] = byts / (ms * 1e-3) / 1e9
+    # back-to-back scans inside one launch (the fit's regime: no launch, no
+    # pipeline fill per scan); L2 flushed before the launch
+    for reps in (1, 2, 8, 32):
+        lib.scx_timing_reset(h)
+        for _ in range(3):
+            l2.add_(1.0)
+            torch.cuda.synchronize()
+            assert lib.scx_risk_prefix_n(h, reps) == 0
+        lib.scx_timing_get(h, 3, C.byref(tot), C.byref(nl))
+        ms = tot.value / max(1, nl.value) / reps
+        out[f"prefix_x{reps}_us"] = ms * 1e3
+        out[f"prefix_x{reps}_gbs"] = byts / (ms * 1e-3) / 1e9
     lib.scx_timing_reset(h)
     for j in range(min(args.p, 16)):
         sx.risk_suffix_gradient_hessian(dd, st, j)

@@ -180,3 +180,30 @@ def test_risk_suffix_mixed_penalties_match_oracle(oracle, ref):
     assert np.allclose(r.objective_trace, want["trace"], rtol=LL_RTOL, atol=0)
     nz = np.count_nonzero(r.beta)
     assert 0 < nz < p, nz  # both kinds of coordinate present at the optimum
+
+
+def test_repeated_scans_in_one_launch_are_identical():
+    """scx_risk_prefix_n (the throughput probe: back-to-back scans inside one
+    launch, as the fit runs them) leaves the same R, Q and tile carries as one
+    scan: the stage / carry-slot sequences continue correctly across scans."""
+    import ctypes as C
+
+    from paper_2310_16238_b200 import _capi, synthetic
+
+    lib = _capi.load()
+    n = 3_000_000
+    syn = synthetic.generate(n, 16, 1500, 0.02, seed=7, device="cuda")
+    dd = sx.upload(syn.sorted_design())
+    assert dd.set_fit_path(0)
+    sx.make_state(dd, np.random.default_rng(3).normal(0, 0.1, 16))
+    nt = (n + 2047) // 2048 + 1
+    got = []
+    for reps in (1, 4):
+        arrs = [np.zeros(n), np.zeros(n), np.zeros(nt), np.zeros(nt)]
+        assert lib.scx_risk_prefix_n(dd.handle, reps) == 0
+        assert lib.scx_debug_risk_arrays(dd.handle, *(_capi.ptr(a, C.c_double) for a in arrs), None) == 0
+        got.append(arrs)
+    for a, b in zip(got[0], got[1]):
+        assert np.array_equal(a, b)
+    assert lib.scx_risk_prefix_n(dd.handle, 0) != 0  # reps >= 1
+    dd.close()
