@@ -305,6 +305,27 @@ def run_small_config(args):
     k1_ms = tot.value / max(1, nl.value)
     lib.scx_timing_enable(dd.handle, 0)
     alg = info["n_rows"] * (8 + info["code_bytes"]) + 4 * float(np.mean(cols[sample]))
+    # the risk-suffix cycle's scan (when the design takes it), L2 flushed
+    rs_on = dd.set_fit_path(0)
+    fit_stats = dd.fit_path_stats()
+    rs_roof = None
+    if rs_on:
+        lib.scx_timing_enable(dd.handle, 1)
+        lib.scx_timing_reset(dd.handle)
+        for _ in range(16):
+            l2buf.add_(1)
+            torch.cuda.synchronize(dev)
+            assert lib.scx_risk_prefix(dd.handle) == 0
+        lib.scx_timing_get(dd.handle, 3, C.byref(tot), C.byref(nl))
+        rs_ms = tot.value / max(1, nl.value)
+        lib.scx_timing_enable(dd.handle, 0)
+        rs_bytes = info["n_rows"] * (8 + info["code_bytes"] + 16)
+        rs_roof = {"bound": "hbm", "achieved": rs_bytes / (rs_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                   "unit": "GB/s", "frac": rs_bytes / (rs_ms * 1e-3) / 1e9 / hbm_peak,
+                   "traffic": None, "kernel": "k_rs_cycle risk scan"
+                   + ("" if chunked.value else " (chunks of whole tiles, carries across CTAs)"),
+                   "avg_launch_ms": rs_ms, "algorithmic_bytes_per_launch": rs_bytes,
+                   "algorithmic_bytes_per_row": 8 + info["code_bytes"] + 16, "peak_source": peak_src}
     del st
     dd.close()
     # e2e: host subject arrays -> (device) lowering + sort + upload -> fit -> beta back
@@ -352,10 +373,16 @@ def run_small_config(args):
                    "device_lower_sort_upload_s": t_build,
                    "l2_flush": "256 MiB write before every timed fit and K1 launch"},
         "fit_wall_s": ms_step / 1e3,
-        "roofline": {"bound": "hbm", "achieved": alg / (k1_ms * 1e-3) / 1e9, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": alg / (k1_ms * 1e-3) / 1e9 / hbm_peak,
-                     "traffic": None, "kernel": "k1_grad_hess", "avg_launch_ms": k1_ms,
-                     "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
+        "fit_path": "risk-suffix cycle" if fit_stats.get("risk_suffix_launches") else "fused-scan cycle",
+        "fit_path_stats": fit_stats,
+        "roofline": dict(rs_roof or {}, k1_fused_scan_per_coordinate={
+            "kernel": "k1_grad_hess", "avg_launch_ms": k1_ms, "algorithmic_bytes_per_launch": alg,
+            "achieved_gbs": alg / (k1_ms * 1e-3) / 1e9, "frac": alg / (k1_ms * 1e-3) / 1e9 / hbm_peak})
+        if rs_roof else
+        {"bound": "hbm", "achieved": alg / (k1_ms * 1e-3) / 1e9, "peak": hbm_peak,
+         "unit": "GB/s", "frac": alg / (k1_ms * 1e-3) / 1e9 / hbm_peak,
+         "traffic": None, "kernel": "k1_grad_hess", "avg_launch_ms": k1_ms,
+         "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": {"value": float(r2.n_evaluations) / e2e_s, "unit": "evals/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * p, "seconds_per_step": e2e_s},

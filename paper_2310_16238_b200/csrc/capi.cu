@@ -146,6 +146,7 @@ void free_design(scx_ctx* ctx) {
                     ctx->vals_d, ctx->tptr_d, ctx->zero_cols_d, d.lasth1, d.ref_act,
                     d.ref_abeg, d.ref_avo, d.ref_ab, d.ref_nact, d.ref_meta,
                     d.chunk_rows, ctx->cols_d, d.rs_CR, d.rs_CQ, d.rs_R, d.rs_Q, d.chunk_k, ctx->col1_d,
+                    d.rs_chunk_nk, d.rs_xagg, d.rs_aligned ? nullptr : d.rs_chunk_rows,
                     d.ell_col, d.ell_val, d.ell_base};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -755,6 +756,13 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
                 CK(dmalloc(&d.chunk_k, ck.size()));
                 CK(cudaMemcpyAsync(d.chunk_k, ck.data(), ck.size() * sizeof(int32_t),
                                    cudaMemcpyHostToDevice, s));
+                std::vector<int32_t> nk(ck.size() - 1);
+                for (size_t c = 0; c + 1 < ck.size(); ++c) nk[c] = ck[c + 1] - ck[c];
+                CK(dmalloc(&d.rs_chunk_nk, nk.size()));
+                CK(cudaMemcpyAsync(d.rs_chunk_nk, nk.data(), nk.size() * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, s));
+                d.rs_chunk_rows = d.chunk_rows;
+                d.rs_aligned = 1;
                 CK(dmalloc(&d.rs_CR, d.ntiles1));
                 CK(dmalloc(&d.rs_CQ, d.ntiles1));
                 CK(cudaMemsetAsync(d.rs_CR, 0, d.ntiles1 * sizeof(double), s));
@@ -765,6 +773,55 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
             }
         }
     }
+    // Few large strata (no stratum-aligned chunking, e.g. the lowered configs
+    // 2-3): the risk-suffix cycle on chunks of whole 2048-row tiles, strata
+    // running across chunk ends (carries meet across CTAs, rs_chunk_carry_in)
+    if (!d.rs_ok) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        if (ctx->sm_budget > 0) sms = std::min(sms, ctx->sm_budget);
+        const int64_t G = sms > 0 ? sms : 148;
+        const int64_t tiles = (n + kK1TileRows - 1) / kK1TileRows;
+        if (k >= 1 && tiles >= 4 * G && G <= 512) {
+            std::vector<int32_t> ch(G + 1), ck(G + 1), nk(G);
+            for (int64_t c = 0; c <= G; ++c)
+                ch[c] = (int32_t)std::min<int64_t>(n, (tiles * c / G) * kK1TileRows);
+            bool fits = true;
+            for (int64_t c = 0; c <= G; ++c) {
+                // the stratum holding row ch[c] (the last one for c = G)
+                const int64_t r = std::min<int64_t>(ch[c], n - 1);
+                ck[c] = (int32_t)(std::upper_bound(offsets, offsets + k + 1, r) - offsets - 1);
+            }
+            for (int64_t c = 0; c < G; ++c) {
+                // strata overlapping the chunk: up to the first starting at or after its end
+                const int32_t e = (int32_t)(std::lower_bound(offsets, offsets + k + 1, (int64_t)ch[c + 1]) - offsets);
+                nk[c] = e - ck[c];
+                const int64_t nt = (ch[c + 1] - 1) / kK1TileRows - ch[c] / kK1TileRows + 1;
+                if (nk[c] < 1 || nk[c] > kRsMaxStrata || nt > kRsTileInfo) fits = false;
+            }
+            if (fits) {
+                CK(dmalloc(&d.rs_chunk_rows, ch.size()));
+                CK(cudaMemcpyAsync(d.rs_chunk_rows, ch.data(), ch.size() * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, s));
+                CK(dmalloc(&d.chunk_k, ck.size()));
+                CK(cudaMemcpyAsync(d.chunk_k, ck.data(), ck.size() * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, s));
+                CK(dmalloc(&d.rs_chunk_nk, nk.size()));
+                CK(cudaMemcpyAsync(d.rs_chunk_nk, nk.data(), nk.size() * sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, s));
+                CK(dmalloc(&d.rs_CR, d.ntiles1));
+                CK(dmalloc(&d.rs_CQ, d.ntiles1));
+                CK(cudaMemsetAsync(d.rs_CR, 0, d.ntiles1 * sizeof(double), s));
+                CK(cudaMemsetAsync(d.rs_CQ, 0, d.ntiles1 * sizeof(double), s));
+                CK(dmalloc(&d.rs_R, d.npad));
+                CK(dmalloc(&d.rs_Q, d.npad));
+                d.nchunks = (int32_t)G;
+                d.rs_aligned = 0;
+                d.rs_ok = 1;
+            }
+        }
+    }
+    if (d.rs_ok) CK(dmalloc(&d.rs_xagg, 4 * std::max<int64_t>(d.nchunks, 1)));
     CK(dmalloc(&d.status, d.ntiles));
     CK(dmalloc(&d.slots, 2 * d.ntiles1 * 8));
     CK(cudaMemsetAsync(d.slots, 0, 2 * d.ntiles1 * 8 * sizeof(double), s));

@@ -370,7 +370,11 @@ struct DesignDev {
     double* rs_Q;             // [npad] within-stratum suffix sum of w/S0^2 from each row
     CUtensorMap tmap_R;
     CUtensorMap tmap_Q;
-    int32_t* chunk_k;         // [nchunks+1] first stratum of each chunk
+    int32_t* chunk_k;         // [nchunks+1] first stratum of each chunk (holding its first row)
+    int32_t* rs_chunk_nk;     // [nchunks] strata of each risk-scan chunk
+    int32_t* rs_chunk_rows;   // [nchunks+1] risk-scan chunks (= chunk_rows when stratum-aligned)
+    int32_t rs_aligned;       // risk-scan chunks start at heads (else whole tiles, carries cross)
+    double* rs_xagg;          // [4 * nchunks] cross-chunk carries (unaligned chunks)
     int32_t rs_ok;            // chunks hold <= kRsMaxStrata strata each
     Xchg x;                   // multi-GPU exchange (x.nranks == 1: single device)
 };

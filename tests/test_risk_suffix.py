@@ -48,6 +48,11 @@ DESIGNS = [
     (1_300_000, 2000, 3, 0.15, 1e9, True),    # value columns, dense
     (1_400_000, 1500, 3, 0.01, 40, True),     # heavy ties (w >= 2, wide codes)
     (1_250_000, 20000, 2, 0.05, 1e9, False),  # small strata (135 per chunk)
+    # few large strata (the lowered configs' shape): chunks of whole tiles,
+    # strata across chunk ends, carries meeting across CTAs
+    (1_400_000, 1, 3, 0.02, 1e9, False),      # one stratum
+    (1_300_000, 7, 3, 0.15, 1e9, True),       # value columns, dense
+    (1_400_000, 20, 3, 0.01, 40, True),       # heavy ties, wide codes
 ]
 
 
@@ -75,6 +80,9 @@ def test_risk_suffix_gradient_matches_oracle(oracle, ref, n, k, p, density, grid
     (1_300_000, 2000, 3, 0.15, 1e9, True, 0.05),
     (1_400_000, 1500, 3, 0.01, 40, True, 0.0),      # unpenalised: Newton on every coordinate
     (1_250_000, 20000, 3, 0.05, 1e9, False, 0.02),
+    (1_300_000, 1, 4, 0.05, 1e9, False, 0.1),       # unaligned chunks: one stratum
+    (1_300_000, 12, 3, 0.15, 1e9, True, 0.05),      # ... value columns, 12 strata
+    (1_400_000, 20, 3, 0.02, 40, False, 0.05),      # ... heavy ties
 ])
 def test_risk_suffix_fit_matches_oracle(oracle, ref, n, k, p, density, grid, values, gfrac):
     a = _design(oracle, ref, n, k, p, density, grid, values, 5 + k)
