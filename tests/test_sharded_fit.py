@@ -100,3 +100,14 @@ def test_per_coordinate_sharded_path_small_design(oracle):
     z = G.load("fits")
     a = G.design_arrays(z, "cfg1_l1_")
     _check(oracle, a, z["cfg1_l1_gamma"], 2, max_cycles=40, expect_rs=False)
+
+
+def test_two_shards_few_large_strata(oracle, ref):
+    """Four large strata: each rank's rows (two whole strata) take the
+    risk-suffix cycle on chunks of whole tiles, the carries meeting across
+    that rank's CTAs, and the partial sums across the ranks."""
+    a = _sim_design(ref, 2_800_000, 4, 4, 9, density=0.03)
+    dd = sx.upload(G.sorted_design(a, values=False))
+    gmax = sx.gamma_max(dd)
+    dd.close()
+    _check(oracle, a, np.full(a["p"], 0.05 * gmax), 2)
