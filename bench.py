@@ -729,6 +729,7 @@ def main():
         e2e_evals.append(r2.n_evaluations)
         dd2.close()
     e2e_value = (float(np.mean(e2e_evals)) / float(np.mean(e2e_times))) if e2e_times else None
+    log(f"[bench] e2e seconds per step {e2e_times}")
 
     # ---- CPU baseline + parity of the benchmarked fit path (rank 0, N=1 only).
     # The reference (oracle/_ref) generates a bounded sample of the same workload

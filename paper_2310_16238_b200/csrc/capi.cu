@@ -1,3 +1,4 @@
+#include <chrono>
 // C-ABI (include/stratcox_b200.h) over the sm_100a kernels in kernels.cu.
 //
 // Host responsibilities only: argument validation with the reference's exact
@@ -531,6 +532,24 @@ struct DevSrc {
     int64_t n_ind;
 };
 
+// Upload phase timing (SCX_UPLOAD_TRACE=1: stream synchronised at each phase,
+// durations on stderr; diagnostics only).
+struct UploadClock {
+    bool on;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t;
+    explicit UploadClock(cudaStream_t st)
+        : on(getenv("SCX_UPLOAD_TRACE") != nullptr), s(st), t(std::chrono::steady_clock::now()) {}
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[scx upload] %-28s %9.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_t* offsets,
                                 const uint8_t* event, const int64_t* tie_end, int64_t p,
                                 const int64_t* col_ptr, const int64_t* row64,
@@ -538,6 +557,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
                                 const DevSrc* dev = nullptr) {
     if (!ctx) return SCX_ERR_VALIDATION;
     cudaSetDevice(ctx->device);
+    UploadClock uc(ctx->stream);
     if (n < 1) return fail(ctx, SCX_ERR_VALIDATION, "dataset has no rows");
     if (k < 1) return fail(ctx, SCX_ERR_VALIDATION, "dataset has no strata");
     if (n > (int64_t)0x7fffffff - kTileRows)
@@ -593,6 +613,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     d.ntiles1 = d.npad / kK1TileRows;
     cudaStream_t s = ctx->stream;
 
+    uc.mark("validation + columns (host)");
     // --- event codes
     uint8_t* event_d = nullptr;
     int64_t* tie_d = nullptr;
@@ -632,6 +653,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         ctx->event_h.assign(event, event + n);
     }
 
+    uc.mark("event codes");
     // --- CSC
     if (dev)
         ctx->rows_d = dev->rows32_d;  // sorted on the device, nnz + 16 entries
@@ -692,6 +714,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
     cudaFree(maxw_d);
     cudaFree(stats_d);
 
+    uc.mark("CSC upload + column stats + tile pointers");
     // --- state + scratch
     CK(dmalloc(&d.D, d.npad));
     CK(dmalloc(&d.eta, d.npad));
@@ -888,10 +911,12 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         ctx->cycle_cols = nz;
     }
     d.x = ctx->x;  // a re-upload keeps the multi-GPU exchange
+    uc.mark("chunks + cycle columns");
     CK(dmalloc(&ctx->zero_cols_d, ctx->zero_cols.size()));
     if (!ctx->zero_cols.empty())
         CK(cudaMemcpyAsync(ctx->zero_cols_d, ctx->zero_cols.data(),
                            ctx->zero_cols.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    uc.mark("zero columns");
     // row-slice copy of the design for the 256-update refresh (skipped, and
     // the tile refresh kept, when the re-sort's scratch does not fit)
     {
@@ -903,6 +928,7 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
             CK(e);
         }
     }
+    uc.mark("row-slice copy (refresh)");
     ctx->nnz = nnz;
     ctx->n_indicator = n_ind;
     ctx->has_design = true;
@@ -911,8 +937,10 @@ static scx_status upload_common(scx_ctx* ctx, int64_t n, int32_t k, const int64_
         free_design(ctx);
         return st;
     }
+    uc.mark("checks");
     // state at beta = 0 (make_state)
     KL(refresh_launches(d), launch_refresh(d, s));
+    uc.mark("initial state");
     return check_device_error(ctx);
 }
 

@@ -1,3 +1,4 @@
+#include <mutex>
 // Device build of the SortedDesign: build_sorted_design,
 // proj/src/data.cpp:68-147, with validate_invariants (data.cpp:27-66) — on the
 // GPU instead of the host.
@@ -738,11 +739,34 @@ using namespace scx;
 
 namespace {
 
+// Scratch of one build. With a stream, stream-ordered allocations from the
+// device's memory pool, which keeps its memory across builds (release
+// threshold raised once per device): a re-upload's multi-GB sort scratch
+// costs no new page mappings.
 struct DevBuf {
     std::vector<void*> ptrs;
+    cudaStream_t st = nullptr;
+    bool pooled = false;
+    DevBuf() = default;
+    explicit DevBuf(cudaStream_t s) : st(s), pooled(true) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        static std::mutex mu;
+        static bool done[64] = {};
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev >= 0 && dev < 64 && !done[dev]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            done[dev] = true;
+        }
+    }
     template <typename T>
     cudaError_t alloc(T** p, size_t count) {
-        cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+        const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+        cudaError_t e = pooled ? cudaMallocAsync((void**)p, bytes, st) : cudaMalloc((void**)p, bytes);
         if (e == cudaSuccess) ptrs.push_back(*p);
         return e;
     }
@@ -751,7 +775,12 @@ struct DevBuf {
         if (it != ptrs.end()) ptrs.erase(it);
     }
     ~DevBuf() {
-        for (void* p : ptrs) cudaFree(p);
+        for (void* p : ptrs) {
+            if (pooled)
+                cudaFreeAsync(p, st);
+            else
+                cudaFree(p);
+        }
     }
 };
 
@@ -1204,7 +1233,7 @@ cudaError_t scx::build_refresh_ell(DesignDev& d, int64_t nnz, bool any_values, c
     cudaMemGetInfo(&free_b, &total_b);
     const size_t need = (size_t)nnz * (16 + 2 * 4 + (any_values ? 10 : 3)) + (size_t)n * 16;
     if (need > free_b / 2) return cudaSuccess;  // leave room for the fit's own scratch
-    DevBuf B;
+    DevBuf B(s);
     uint32_t *keys, *keys2, *ent, *ent2;
     if (B.alloc(&keys, nnz) || B.alloc(&keys2, nnz) || B.alloc(&ent, nnz) || B.alloc(&ent2, nnz))
         return cudaGetLastError();
