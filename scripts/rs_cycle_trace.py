@@ -14,7 +14,7 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["SCX_K1_DBG"] = "256"
+os.environ["SCX_K1_DBG"] = os.environ.get("SCX_K1_DBG", "256")
 os.environ.setdefault("SCX_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2310_16238_b200", "libstratcox_b200_trace.so"))
 
 
@@ -61,6 +61,14 @@ def main():
     for k, v in ph.items():
         print(f"  {k:22s} {int(v):>10d} cycles {int(v) / max(1, n):8.0f}/round  {v / max(1, tot):.1%}"
               f"  n={cnt[k]} {int(v) / max(1, cnt[k]) / 1.965e3:.1f} us each")
+    r0 = tr[0][:n]
+    if r0[:, 0].any():  # SCX_K1_DBG bit 1024: inside the gradient rounds
+        ok = (r0[:, 0] > 0) & (t[:n, 0] > 0)
+        setup = (r0[ok, 0] - t[:n, 0][ok]) / 1.965e3
+        ent = (r0[ok, 1] - r0[ok, 0]) / 1.965e3
+        bs = (r0[ok, 2] - r0[ok, 1]) / 1.965e3
+        print(f"  grad round inside: setup {setup.mean():.1f} us, entries {ent.mean():.1f} us, "
+              f"block sum {bs.mean():.1f} us (n={int(ok.sum())})")
     print("stats", dd.fit_path_stats(), "cycles", r.cycles_used)
 
 
