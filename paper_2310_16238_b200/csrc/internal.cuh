@@ -74,9 +74,10 @@ struct DevCtl {
     unsigned int done;
     unsigned int epoch;
     unsigned int pad0;
-    // software grid barrier for cooperative kernels
-    unsigned int bar_count;
-    unsigned int bar_gen;
+    // software grid barrier for cooperative kernels: low 32 bits arrivals,
+    // high 32 bits generation (one word: the last arrival resets the count and
+    // advances the generation with one atomic)
+    unsigned long long bar;
     // error word
     int err_kind;
     int pad1;
@@ -220,15 +221,16 @@ __device__ __forceinline__ void st_release(unsigned int* p, uint32_t v) {
 __device__ __forceinline__ void grid_sync(DevCtl* ctl) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned int* gen = &ctl->bar_gen;
-        const unsigned int g = *gen;
-        __threadfence();
-        if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
-            ctl->bar_count = 0;
-            __threadfence();
-            atomicAdd(&ctl->bar_gen, 1u);
+        unsigned long long* w = &ctl->bar;
+        __threadfence();  // this CTA's writes before its arrival
+        const unsigned long long old = atomicAdd(w, 1ull);
+        if ((unsigned int)old == gridDim.x - 1) {
+            // last arrival: count back to 0 and generation + 1 in one atomic, so
+            // no CTA of the next barrier can arrive before the reset
+            atomicAdd(w, (1ull << 32) - gridDim.x);
         } else {
-            while (*gen == g) {
+            const unsigned int gen = (unsigned int)(old >> 32);
+            while ((unsigned int)(*((volatile unsigned long long*)w) >> 32) == gen) {
             }
         }
         __threadfence();
