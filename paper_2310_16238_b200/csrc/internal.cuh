@@ -106,6 +106,7 @@ struct DevCtl {
     int resume;     // cycle kernel: coordinates done before it stopped for a refresh (0: ran to the end)
     int rs_reason;  // risk-suffix cycle: why it stopped (RsStop)
     unsigned long long xseq;  // multi-GPU: device exchanges done so far (the same on every rank)
+    unsigned long long bar2;  // second grid-barrier word (split arrive / wait, see grid_arrive)
 };
 
 // Why a risk-suffix cycle launch returned before its last coordinate.
@@ -236,6 +237,23 @@ __device__ __forceinline__ void grid_sync(DevCtl* ctl) {
         __threadfence();
     }
     __syncthreads();
+}
+
+// Split grid barrier on a word of the same layout (thread 0 only): arrive after
+// the CTA's writes, returning the generation; wait until it advances. Every CTA
+// arrives at every such barrier; waiting is optional, so a CTA that did not wait
+// must pass a full grid_sync on another word before it arrives again (the
+// arrivals of one generation then all precede it).
+__device__ __forceinline__ unsigned int grid_arrive(unsigned long long* w) {
+    __threadfence();
+    const unsigned long long old = atomicAdd(w, 1ull);
+    if ((unsigned int)old == gridDim.x - 1) atomicAdd(w, (1ull << 32) - gridDim.x);
+    return (unsigned int)(old >> 32);
+}
+__device__ __forceinline__ void grid_wait(unsigned long long* w, unsigned int gen) {
+    while ((unsigned int)(*((volatile unsigned long long*)w) >> 32) == gen) {
+    }
+    __threadfence();
 }
 
 __device__ __forceinline__ void set_error(DevCtl* ctl, int kind, long long idx) {
