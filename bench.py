@@ -330,7 +330,7 @@ def run_small_config(args):
     dd.close()
     # e2e: host subject arrays -> (device) lowering + sort + upload -> fit -> beta back
     e2e_runs = []
-    for _ in range(2):
+    for _ in range(3):
         t0 = time.perf_counter()
         dd2 = build()
         r2 = sx.ccd_fit(dd2, pen, cfg)
