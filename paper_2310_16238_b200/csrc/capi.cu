@@ -1583,6 +1583,30 @@ scx_status scx_gamma_max(scx_ctx* ctx, const double* gamma_template, double* out
     std::vector<double> zero(d.p, 0.0);
     if (scx_status s = scx_make_state(ctx, zero.data())) return s;
     double best = 0.0;
+    const std::vector<ColArgs>& cc = ctx->cycle_cols;  // the non-empty columns (cols_d)
+    if (ctx->nranks == 1 && ctx->fit_path == 0 && d.rs_ok && d.k1_mode != 1 && !cc.empty()) {
+        // risk-suffix path (eta = 0 here): one scan, then every column's
+        // g' = -lin + sum a R in gradient rounds of one launch (O(nnz) gathers
+        // instead of one O(N) pass per column)
+        double* gout = nullptr;
+        CK(dmalloc(&gout, cc.size()));
+        std::vector<double> g(cc.size());
+        cudaError_t e = launch_rs_cycle(d, ctx->cols_d, (int)cc.size(), 3, ctx->stream, gout);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(g.data(), gout, cc.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        cudaFree(gout);
+        CK(e);
+        ++ctx->launches;
+        if (scx_status s = check_device_error(ctx, -1)) return s;
+        for (size_t i = 0; i < cc.size(); ++i) {
+            if (gamma_template && gamma_template[cc[i].j] <= 0.0) continue;
+            best = dmax(best, std::fabs(g[i]));
+        }
+        *out = best;
+        return SCX_OK;
+    }
     for (int64_t j = 0; j < d.p; ++j) {
         if (gamma_template && gamma_template[j] <= 0.0) continue;
         if (ctx->cols[j].nnz == 0) continue;

@@ -404,9 +404,10 @@ enum K1Mode : int { kK1Eval = 0, kK1Fit = 1, kK1Diag = 2, kK1Partial = 3 };
 cudaError_t launch_k1(const DesignDev& d, const ColArgs& col, int mode, cudaStream_t s);
 cudaError_t k1_trace_copy(long long* out);
 // risk-suffix CCD cycle over cols_d[0..ncols): mode 0 fit, 1 evaluate cols_d[0]
-// only (g, h into ctl), 2 risk scan only (ncols back-to-back scans: throughput probe)
+// only (g, h into ctl), 2 risk scan only (ncols back-to-back scans: throughput probe),
+// 3 g' of every column at the current state into gout[0..ncols) (gamma_max)
 cudaError_t launch_rs_cycle(const DesignDev& d, const ColArgs* cols_d, int ncols, int mode,
-                            cudaStream_t s);
+                            cudaStream_t s, double* gout = nullptr);
 // one CCD cycle in one cooperative launch over cols_d[0..ncols) (all of one
 // kind: indicator or value columns)
 cudaError_t launch_cycle(const DesignDev& d, const ColArgs* cols_d, int ncols, bool indicator,

@@ -215,3 +215,24 @@ def test_repeated_scans_in_one_launch_are_identical():
         assert np.array_equal(a, b)
     assert lib.scx_risk_prefix_n(dd.handle, 0) != 0  # reps >= 1
     dd.close()
+
+
+@pytest.mark.parametrize("n,k,p,density,grid,values", DESIGNS)
+def test_risk_suffix_gamma_max_matches_oracle(oracle, ref, n, k, p, density, grid, values):
+    """gamma_max (resample.hpp:38-39) on the chunked layout runs as one
+    risk-suffix launch (every column's g' at beta = 0 in gradient rounds): the
+    oracle's value and the per-coordinate fused-scan path's within 1e-10, and a
+    penalty template with unpenalised columns excludes them the same way."""
+    a = _design(oracle, ref, n, k, p, density, grid, values, 99)
+    d = oracle.design(a)
+    dd = upload(a, values=values)
+    assert dd.set_fit_path(0)
+    want = oracle.gamma_max(d)
+    got = sx.gamma_max(dd)
+    assert G.close_rel(got, want, GH_RTOL), (got, want)
+    tmpl = np.ones(p)
+    tmpl[0] = 0.0  # column 0 unpenalised: left out of the max
+    g_t = sx.gamma_max(dd, sx.PenaltySpec(tmpl))
+    dd.set_fit_path(1)
+    assert G.close_rel(sx.gamma_max(dd), want, GH_RTOL)
+    assert G.close_rel(g_t, sx.gamma_max(dd, sx.PenaltySpec(tmpl)), GH_RTOL)
